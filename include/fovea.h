@@ -1,0 +1,179 @@
+/*
+ * fovea.h -- C ABI of libfovea.so: blockwise foveated rendering on one B200 (sm_100a).
+ *
+ * The reference (foveakit 0.1.0, pure Python) has no FFI seam; its boundary for this
+ * path is the Python API re-exported at pkg/src/foveakit/__init__.py:13-62.  Each entry
+ * point below names the reference function(s) it replaces (file:line under
+ * /root/reference/pkg/src/foveakit/).  paper_2012_08655_b200/_native.py is the ctypes
+ * binding; INTEGRATION.md shows the stub a foveakit maintainer would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every function returns an int status
+ *     (FK_OK / FK_EINVAL -> ValueError / FK_ECUDA, FK_ENOMEM -> RuntimeError) and
+ *     leaves a message retrievable with fk_last_error().
+ *   - "dev" pointers are device memory on the handle's GPU, "host" pointers are host
+ *     memory.  `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - frames are row-major interleaved [N][H][W][C], C in {1,3}, uint8 or float32
+ *     (imaging.py:19-39); fixations are double (x, y) pairs in pixels.
+ *   - all functions are re-entrant across handles; one handle serves one device and may
+ *     be used from one thread at a time (blockwise.py:13-15, SPEC.md "Concurrency Model").
+ *   - there is no CPU fallback: without a CUDA device fk_create fails with FK_ECUDA.
+ */
+#ifndef FOVEA_H_
+#define FOVEA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FK_OK 0
+#define FK_EINVAL 1 /* bad argument: the Python shim raises ValueError(fk_last_error) */
+#define FK_ECUDA 2  /* CUDA runtime failure or no device */
+#define FK_ENOMEM 3
+
+#define FK_ABI_VERSION 1
+
+typedef struct fk_handle fk_handle; /* one GPU: canonical tap LUT, streams, scratch */
+typedef struct fk_plan fk_plan;     /* device-resident plans for up to max_frames frames */
+
+/*
+ * POD mirror of FoveationParams (retinal.py:34-44) plus the scalars the reference
+ * evaluates on the host with Python's math module; they are passed in so that the
+ * device sigma map is bit-identical to the reference's:
+ *   log_inv_ct0 = math.log(1.0 / ct0)                      retinal.py:129
+ *   two_pi      = 2.0 * math.pi                            retinal.py:155
+ *   fmax        = params.max_cpd()                         retinal.py:63-65
+ *   d_corner    = math.hypot(w / 2.0, h / 2.0)             retinal.py:111
+ */
+typedef struct fk_params {
+    double alpha;
+    double e2;
+    double ct0;
+    double e_corner;
+    double strength;
+    double log_inv_ct0;
+    double two_pi;
+    double fmax;
+    double d_corner;
+    int32_t fragment_size; /* >= 4 (blockwise.py:46-47) */
+    /* 1: shift from the fixation (plan(..., use_shift=True), blockwise.py:207);
+     * 0: no shift; 2: explicit (shift_x, shift_y), as build_sigma_field's `shift`
+     * argument allows (retinal.py:159-161). */
+    int32_t use_shift;
+    int32_t shift_x, shift_y;
+} fk_params;
+
+/* Host-side view of one frame's plan, filled by fk_plan_read (arrays are caller-owned,
+ * each with room for fk_plan_cell_capacity() entries; NULL pointers are skipped). */
+typedef struct fk_plan_view {
+    int32_t shift_x, shift_y; /* compute_fragment_shift, blockwise.py:39-51 */
+    int32_t grid_w, grid_h;   /* len(fragment_spans(...)), tiling.py:15-28 */
+    int32_t foveal_gy, foveal_gx; /* cell_of(...), tiling.py:36-39, blockwise.py:128 */
+    int32_t max_length;       /* largest tap count used by the frame */
+    int32_t status;           /* 0 ok; 1 fixation outside image (retinal.py:73-74) */
+    double *sigma;            /* [grid_h*grid_w] SigmaField.sigma, retinal.py:159-177 */
+    int32_t *raw_length;      /* filter_length(sigma), filters.py:20-27 */
+    int32_t *length;          /* same with the foveal cell forced to 1, blockwise.py:129-130 */
+} fk_plan_view;
+
+typedef struct fk_device_info {
+    int32_t device;
+    int32_t sm_count;
+    int32_t cc_major, cc_minor;
+    int32_t clock_khz;       /* max SM clock */
+    int32_t l2_bytes;
+    int64_t global_mem_bytes;
+    int32_t max_smem_optin;  /* bytes of shared memory per CTA (opt-in) */
+    char name[64];
+} fk_device_info;
+
+/* ---- lifecycle ----------------------------------------------------------------- */
+int fk_abi_version(void);
+int fk_device_count(int *count);
+int fk_create(int device, fk_handle **out);
+int fk_destroy(fk_handle *h);
+const char *fk_last_error(const fk_handle *h); /* h may be NULL: last error of this thread */
+int fk_get_device_info(fk_handle *h, fk_device_info *out);
+
+/* ---- Gaussian tap LUT ---------------------------------------------------------- */
+/* Replaces gaussian_filter_1d / _bank_from_lengths (filters.py:30-38,77-85): builds, on
+ * the device, the taps of every odd length L <= max_length at the representative
+ * sigma = L / 6.  Filter L occupies [r*r, r*r + L) of the table, r = (L-1)/2.
+ * fk_create builds the table up to 255 taps; planning grows it when needed. */
+int fk_build_lut(fk_handle *h, int max_length, void *stream);
+int fk_lut_max_length(fk_handle *h, int *max_length);
+/* Copy the fp64 taps of one odd length to the host (FilterBank.filters). */
+int fk_lut_read(fk_handle *h, int length, double *taps_host);
+
+/* ---- planning: shift -> sigma field -> tap counts -> foveal cell ----------------- */
+int fk_plan_create(fk_handle *h, int width, int height, int fragment_size,
+                   int max_frames, fk_plan **out);
+int fk_plan_destroy(fk_plan *p);
+int fk_plan_cell_capacity(const fk_plan *p); /* per-frame stride of the cell arrays */
+
+/* Replaces, for n_frames frames at once: compute_fragment_shift (blockwise.py:39-51),
+ * fragment_spans / span_midpoints / cell_of (tiling.py:15-39), eccentricity_of,
+ * cutoff_cpd, cutoff_cpp, sigma_at, build_sigma_field (retinal.py:97-177),
+ * filter_length (filters.py:20-27) and the foveal forcing of build_blur_grid
+ * (blockwise.py:107-133).  fix_xy holds n_frames (x, y) pairs, on the host
+ * (fix_on_device = 0, copied stream-ordered) or already on the device. */
+int fk_plan_model(fk_plan *p, const fk_params *params, int n_frames, const double *fix_xy,
+                  int fix_on_device, void *stream);
+
+/* Replaces render()'s use of an arbitrary (BlurGrid, FilterBank) pair
+ * (blockwise.py:156-186) for ONE frame: the caller supplies the shift, the per-cell tap
+ * counts (odd, >= 1) and offsets into `coeffs` (FilterBank.cumulative_sizes layout,
+ * filters.py:41-49).  All arrays are host memory; grid dims must match the tiling
+ * (else FK_EINVAL, the reference's "does not match image" error). */
+int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_h,
+                     const int32_t *length, const int32_t *offset, const double *coeffs,
+                     int n_coeffs, void *stream);
+
+/* Synchronising read-back of one frame's plan (for BlurGrid / SigmaField objects). */
+int fk_plan_read(fk_plan *p, int frame, fk_plan_view *out, void *stream);
+/* Read-back of tap counts for frames [first, first+count): lengths_host is
+ * [count][cell_capacity], meta_host is [count][8] =
+ * {shift_x, shift_y, grid_w, grid_h, foveal_gy, foveal_gx, max_length, status}. */
+int fk_plan_read_lengths(fk_plan *p, int first, int count, int32_t *lengths_host,
+                         int32_t *meta_host, void *stream);
+
+/* ---- render: the per-fragment separable blur -------------------------------------- */
+/* Replaces render / _render_cell (blockwise.py:136-186) + quantize_u8 (convolve.py:9-15)
+ * for n_frames frames planned in `p`.  in/out are device pointers, [n][H][W][C]. */
+int fk_render_u8(fk_handle *h, const fk_plan *p, const uint8_t *in_dev, uint8_t *out_dev,
+                 int n_frames, int channels, void *stream);
+/* Same arithmetic on float32 frames, result left unquantised (BASELINE config 5). */
+int fk_render_f32(fk_handle *h, const fk_plan *p, const float *in_dev, float *out_dev,
+                  int n_frames, int channels, void *stream);
+
+/* Kernel selection for tests and profiling: 0 = auto (fast path with generic fallback),
+ * 1 = force the generic kernel.  Returns the previous value. */
+int fk_set_kernel_variant(fk_handle *h, int variant);
+/* Number of kernel launches issued through this handle so far (bench "gpu_launches"). */
+int64_t fk_launch_count(const fk_handle *h);
+
+/* ---- foveate: host frames in, host frames out (the call a foveakit user makes) ----- */
+/* Replaces foveate() (blockwise.py:223-243) for a batch held in HOST memory: pipelines
+ * H2D copy -> plan -> render -> D2H copy over internal streams in chunks of
+ * `chunk_frames` (0 = pick).  Pinned buffers (fk_host_alloc) overlap fully. */
+int fk_foveate_host_u8(fk_handle *h, const fk_params *params, int width, int height,
+                       int channels, int n_frames, const double *fix_xy_host,
+                       const uint8_t *in_host, uint8_t *out_host, int chunk_frames);
+int fk_foveate_host_f32(fk_handle *h, const fk_params *params, int width, int height,
+                        int channels, int n_frames, const double *fix_xy_host,
+                        const float *in_host, float *out_host, int chunk_frames);
+int fk_host_alloc(size_t bytes, void **out); /* pinned host memory */
+int fk_host_free(void *ptr);
+
+/* ---- measurement helpers ------------------------------------------------------------ */
+/* Dependent-free FFMA loop on every SM; returns achieved FP32 TFLOP/s (2 flop per FMA)
+ * measured with CUDA events.  The roofline denominator when it is FP32-bound. */
+int fk_measure_fp32_peak(fk_handle *h, double *tflops, double *ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FOVEA_H_ */

@@ -1,0 +1,623 @@
+/*
+ * fk_api.cu -- the C ABI of libfovea.so (include/fovea.h): handles, plans, LUT
+ * management, render dispatch and the host-buffer pipeline.  No torch types; the
+ * Python shim passes raw pointers (tensor.data_ptr(), numpy ctypes pointers).
+ */
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "fk_internal.h"
+
+static thread_local std::string g_err;
+
+int fk_fail(fk_handle *h, int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    if (h) h->err = buf;
+    return code;
+}
+
+int fk_cuda_fail(fk_handle *h, cudaError_t e, const char *what)
+{
+    int code = (e == cudaErrorMemoryAllocation) ? FK_ENOMEM : FK_ECUDA;
+    return fk_fail(h, code, "CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+}
+
+static inline cudaStream_t as_stream(void *s) { return (cudaStream_t)s; }
+
+/* Host evaluation of the sigma chain (retinal.py:112-155) at distance d, used only to
+ * bound the tap count before launching; the authoritative values come from the device. */
+static double fk_sigma_at_distance(const fk_params *p, double d)
+{
+    double e = d / p->d_corner * p->e_corner;
+    double fdeg = p->e2 / (p->alpha * (e + p->e2)) * p->log_inv_ct0;
+    double fpix = 0.5 * fdeg / p->fmax;
+    return p->strength / (p->two_pi * fpix);
+}
+
+static int fk_length_of_sigma(double sigma)
+{
+    if (!(sigma >= 0.0) || !std::isfinite(sigma)) return -1;
+    double n6 = std::ceil(6.0 * sigma);
+    if (n6 > 1.0e7) return -1;
+    int n = n6 < 1.0 ? 1 : (int)n6;
+    return (n & 1) ? n : n + 1;
+}
+
+extern "C" {
+
+int fk_abi_version(void) { return FK_ABI_VERSION; }
+
+int fk_device_count(int *count)
+{
+    if (!count) return fk_fail(nullptr, FK_EINVAL, "count is NULL");
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fk_cuda_fail(nullptr, e, "cudaGetDeviceCount");
+    }
+    return FK_OK;
+}
+
+const char *fk_last_error(const fk_handle *h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int fk_create(int device, fk_handle **out)
+{
+    if (!out) return fk_fail(nullptr, FK_EINVAL, "out is NULL");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fk_fail(nullptr, FK_ECUDA,
+                       "no CUDA device available (%s); libfovea has no CPU fallback",
+                       e != cudaSuccess ? cudaGetErrorString(e) : "device count is 0");
+    if (device < 0 || device >= n)
+        return fk_fail(nullptr, FK_EINVAL, "device %d outside [0, %d)", device, n);
+    fk_handle *h = new (std::nothrow) fk_handle();
+    if (!h) return fk_fail(nullptr, FK_ENOMEM, "out of host memory");
+    h->device = device;
+    FK_CUDA(h, cudaSetDevice(device));
+    e = cudaGetDeviceProperties(&h->prop, device);
+    if (e != cudaSuccess) {
+        int rc = fk_cuda_fail(nullptr, e, "cudaGetDeviceProperties");
+        delete h;
+        return rc;
+    }
+    if (h->prop.major < 10) {
+        int rc = fk_fail(nullptr, FK_ECUDA, "device %d is sm_%d%d; libfovea is built for sm_100a only",
+                         device, h->prop.major, h->prop.minor);
+        delete h;
+        return rc;
+    }
+    for (int i = 0; i < fk_handle::kStreams; i++) {
+        e = cudaStreamCreateWithFlags(&h->streams[i], cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            int rc = fk_cuda_fail(nullptr, e, "cudaStreamCreate");
+            fk_destroy(h);
+            return rc;
+        }
+    }
+    int rc = fk_build_lut(h, FK_LUT_DEFAULT_MAX, nullptr);
+    if (rc != FK_OK) {
+        g_err = h->err;
+        fk_destroy(h);
+        return rc;
+    }
+    cudaStreamSynchronize(nullptr);
+    *out = h;
+    return FK_OK;
+}
+
+static void fk_release_stage(fk_handle *h)
+{
+    for (int i = 0; i < fk_handle::kStreams; i++) {
+        if (h->stage_in[i]) cudaFree(h->stage_in[i]);
+        if (h->stage_out[i]) cudaFree(h->stage_out[i]);
+        if (h->stage_plan[i]) fk_plan_destroy(h->stage_plan[i]);
+        h->stage_in[i] = h->stage_out[i] = nullptr;
+        h->stage_plan[i] = nullptr;
+    }
+    h->stage_bytes = 0;
+    h->stage_frames = 0;
+}
+
+int fk_destroy(fk_handle *h)
+{
+    if (!h) return FK_OK;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    fk_release_stage(h);
+    for (int i = 0; i < fk_handle::kStreams; i++)
+        if (h->streams[i]) cudaStreamDestroy(h->streams[i]);
+    if (h->lut64) cudaFree(h->lut64);
+    if (h->lut32) cudaFree(h->lut32);
+    if (h->probe) cudaFree(h->probe);
+    delete h;
+    return FK_OK;
+}
+
+int fk_get_device_info(fk_handle *h, fk_device_info *out)
+{
+    if (!h || !out) return fk_fail(h, FK_EINVAL, "NULL argument");
+    memset(out, 0, sizeof *out);
+    out->device = h->device;
+    out->sm_count = h->prop.multiProcessorCount;
+    out->cc_major = h->prop.major;
+    out->cc_minor = h->prop.minor;
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, h->device);
+    out->clock_khz = khz;
+    out->l2_bytes = h->prop.l2CacheSize;
+    out->global_mem_bytes = (int64_t)h->prop.totalGlobalMem;
+    out->max_smem_optin = (int32_t)h->prop.sharedMemPerBlockOptin;
+    snprintf(out->name, sizeof out->name, "%.63s", h->prop.name);
+    return FK_OK;
+}
+
+/* ------------------------------------------------------------------------- LUT */
+int fk_build_lut(fk_handle *h, int max_length, void *stream)
+{
+    if (!h) return fk_fail(nullptr, FK_EINVAL, "handle is NULL");
+    if (max_length < 1 || max_length > 8191)
+        return fk_fail(h, FK_EINVAL, "LUT max_length %d outside [1, 8191]", max_length);
+    if ((max_length & 1) == 0) max_length += 1;
+    if (max_length <= h->lut_max) return FK_OK;
+    FK_CUDA(h, cudaSetDevice(h->device));
+    /* Growing replaces the table: make sure nothing in flight still reads the old one. */
+    if (h->lut32) FK_CUDA(h, cudaDeviceSynchronize());
+    const size_t rr = (size_t)(max_length - 1) / 2 + 1;
+    const size_t n = rr * rr;
+    double *l64 = nullptr;
+    float *l32 = nullptr;
+    FK_CUDA(h, cudaMalloc(&l64, n * sizeof(double)));
+    cudaError_t e = cudaMalloc(&l32, n * sizeof(float));
+    if (e != cudaSuccess) {
+        cudaFree(l64);
+        return fk_cuda_fail(h, e, "cudaMalloc(lut32)");
+    }
+    e = fk_launch_build_lut(l64, l32, max_length, as_stream(stream));
+    h->launches++;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(as_stream(stream));
+    if (e != cudaSuccess) {
+        cudaFree(l64);
+        cudaFree(l32);
+        return fk_cuda_fail(h, e, "fk_lut_kernel");
+    }
+    if (h->lut64) cudaFree(h->lut64);
+    if (h->lut32) cudaFree(h->lut32);
+    h->lut64 = l64;
+    h->lut32 = l32;
+    h->lut_max = max_length;
+    return FK_OK;
+}
+
+int fk_lut_max_length(fk_handle *h, int *max_length)
+{
+    if (!h || !max_length) return fk_fail(h, FK_EINVAL, "NULL argument");
+    *max_length = h->lut_max;
+    return FK_OK;
+}
+
+int fk_lut_read(fk_handle *h, int length, double *taps_host)
+{
+    if (!h || !taps_host) return fk_fail(h, FK_EINVAL, "NULL argument");
+    if (length < 1 || (length & 1) == 0)
+        return fk_fail(h, FK_EINVAL, "tap count must be odd and >= 1, got %d", length);
+    int rc = fk_build_lut(h, length, nullptr);
+    if (rc != FK_OK) return rc;
+    const size_t r = (size_t)(length - 1) / 2;
+    FK_CUDA(h, cudaSetDevice(h->device));
+    FK_CUDA(h, cudaMemcpy(taps_host, h->lut64 + r * r, (size_t)length * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    return FK_OK;
+}
+
+/* ------------------------------------------------------------------------ plans */
+int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int max_frames,
+                   fk_plan **out)
+{
+    if (!h || !out) return fk_fail(h, FK_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (width < 1 || height < 1)
+        return fk_fail(h, FK_EINVAL, "image dimensions must be positive, got %dx%d", width, height);
+    if (fragment_size < 4)
+        return fk_fail(h, FK_EINVAL, "fragment_size must be >= 4, got %d", fragment_size);
+    if (max_frames < 1) return fk_fail(h, FK_EINVAL, "max_frames must be >= 1");
+    FK_CUDA(h, cudaSetDevice(h->device));
+    fk_plan *p = new (std::nothrow) fk_plan();
+    if (!p) return fk_fail(h, FK_ENOMEM, "out of host memory");
+    p->h = h;
+    p->max_frames = max_frames;
+    const int gwm = (width + fragment_size - 1) / fragment_size + 1;
+    const int ghm = (height + fragment_size - 1) / fragment_size + 1;
+    fk_plan_dev &d = p->d;
+    d.width = width;
+    d.height = height;
+    d.fragment = fragment_size;
+    d.cap = gwm * ghm;
+    const size_t cells = (size_t)max_frames * d.cap;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&d.sigma, cells * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&d.raw_length, cells * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.length, cells * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.offset, cells * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.order, cells * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.meta, (size_t)max_frames * FK_META_WORDS * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&p->fix_dev, (size_t)max_frames * 2 * sizeof(double));
+    if (e != cudaSuccess) {
+        fk_plan_destroy(p);
+        return fk_cuda_fail(h, e, "cudaMalloc(plan)");
+    }
+    d.taps = h->lut32;
+    *out = p;
+    return FK_OK;
+}
+
+int fk_plan_destroy(fk_plan *p)
+{
+    if (!p) return FK_OK;
+    if (p->h) cudaSetDevice(p->h->device);
+    cudaFree(p->d.sigma);
+    cudaFree(p->d.raw_length);
+    cudaFree(p->d.length);
+    cudaFree(p->d.offset);
+    cudaFree(p->d.order);
+    cudaFree(p->d.meta);
+    cudaFree(p->fix_dev);
+    cudaFree(p->custom_taps);
+    delete p;
+    return FK_OK;
+}
+
+int fk_plan_cell_capacity(const fk_plan *p) { return p ? p->d.cap : 0; }
+
+int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *fix_xy,
+                  int fix_on_device, void *stream)
+{
+    if (!p || !prm || !fix_xy) return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");
+    fk_handle *h = p->h;
+    if (n_frames < 1 || n_frames > p->max_frames)
+        return fk_fail(h, FK_EINVAL, "n_frames %d outside [1, %d]", n_frames, p->max_frames);
+    if (prm->fragment_size != p->d.fragment)
+        return fk_fail(h, FK_EINVAL, "params.fragment_size %d differs from the plan's %d",
+                       prm->fragment_size, p->d.fragment);
+    /* FoveationParams.__post_init__ (retinal.py:46-61) re-checked at the ABI */
+    if (!(prm->alpha > 0) || !(prm->e2 > 0) || !(prm->ct0 > 0 && prm->ct0 < 1) ||
+        !(prm->e_corner >= 0) || !(prm->strength >= 0) || !(prm->fmax > 0) ||
+        !(prm->d_corner > 0) || !std::isfinite(prm->log_inv_ct0) || !(prm->two_pi > 0))
+        return fk_fail(h, FK_EINVAL, "invalid foveation parameters");
+    if (prm->use_shift == 2 && (prm->shift_x < 0 || prm->shift_x >= prm->fragment_size ||
+                                prm->shift_y < 0 || prm->shift_y >= prm->fragment_size))
+        return fk_fail(h, FK_EINVAL, "offset (%d, %d) outside [0, %d)", prm->shift_x,
+                       prm->shift_y, prm->fragment_size);
+    const int W = p->d.width, H = p->d.height;
+    /* Upper bound of the tap count: sigma grows with distance, and no fragment midpoint
+     * is farther from a fixation than the farthest image corner. */
+    double dmax = 0.0;
+    if (fix_on_device) {
+        dmax = std::hypot((double)W, (double)H);
+    } else {
+        for (int i = 0; i < n_frames; i++) {
+            double fx = fix_xy[2 * i], fy = fix_xy[2 * i + 1];
+            if (!(fx >= 0 && fx < W && fy >= 0 && fy < H))
+                return fk_fail(h, FK_EINVAL, "fixation (%g, %g) outside %dx%d image", fx, fy, W, H);
+            double ddx = fx > W - fx ? fx : W - fx, ddy = fy > H - fy ? fy : H - fy;
+            double d = std::hypot(ddx, ddy);
+            dmax = d > dmax ? d : dmax;
+        }
+    }
+    int bound = fk_length_of_sigma(fk_sigma_at_distance(prm, dmax));
+    if (bound < 0 || bound + 2 > 8191)
+        return fk_fail(h, FK_EINVAL, "sigma values must be finite and >= 0 and need <= 8191 taps");
+    bound += 2; /* the device value is authoritative; leave one odd step of slack */
+    FK_CUDA(h, cudaSetDevice(h->device));
+    if (bound > h->lut_max) {
+        int rc = fk_build_lut(h, bound, stream);
+        if (rc != FK_OK) return rc;
+    }
+    cudaStream_t s = as_stream(stream);
+    const double *fix_dev = fix_xy;
+    if (!fix_on_device) {
+        FK_CUDA(h, cudaMemcpyAsync(p->fix_dev, fix_xy, (size_t)n_frames * 2 * sizeof(double),
+                                   cudaMemcpyHostToDevice, s));
+        fix_dev = p->fix_dev;
+    }
+    p->d.taps = h->lut32;
+    p->custom = 0;
+    FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, s));
+    h->launches++;
+    p->n_frames = n_frames;
+    p->bound_length = bound;
+    return FK_OK;
+}
+
+int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_h,
+                     const int32_t *length, const int32_t *offset, const double *coeffs,
+                     int n_coeffs, void *stream)
+{
+    if (!p || !length || !offset || !coeffs)
+        return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");
+    fk_handle *h = p->h;
+    const fk_plan_dev &d = p->d;
+    const int F = d.fragment;
+    if (shift_x < 0 || shift_x >= F || shift_y < 0 || shift_y >= F)
+        return fk_fail(h, FK_EINVAL, "shift (%d, %d) outside [0, %d)", shift_x, shift_y, F);
+    const int gw = fk_span_count(d.width, F, shift_x), gh = fk_span_count(d.height, F, shift_y);
+    if (gw != grid_w || gh != grid_h) /* blockwise.py:168-169 */
+        return fk_fail(h, FK_EINVAL, "grid (%d, %d) does not match image %dx%d", grid_h, grid_w,
+                       d.width, d.height);
+    const int n = gw * gh;
+    int lmax = 1;
+    for (int i = 0; i < n; i++) {
+        if (length[i] < 1 || (length[i] & 1) == 0)
+            return fk_fail(h, FK_EINVAL, "filter lengths must be odd and >= 1, got %d", length[i]);
+        if (offset[i] < 0 || offset[i] + length[i] > n_coeffs)
+            return fk_fail(h, FK_EINVAL, "grid references taps outside the bank");
+        lmax = length[i] > lmax ? length[i] : lmax;
+    }
+    if (lmax > 8191) return fk_fail(h, FK_EINVAL, "filters longer than 8191 taps are not supported");
+    FK_CUDA(h, cudaSetDevice(h->device));
+    cudaStream_t s = as_stream(stream);
+    if (n_coeffs > p->custom_cap) {
+        FK_CUDA(h, cudaStreamSynchronize(s));
+        cudaFree(p->custom_taps);
+        p->custom_taps = nullptr;
+        FK_CUDA(h, cudaMalloc(&p->custom_taps, (size_t)n_coeffs * sizeof(float)));
+        p->custom_cap = n_coeffs;
+    }
+    std::vector<float> taps32((size_t)n_coeffs);
+    for (int i = 0; i < n_coeffs; i++) taps32[i] = (float)coeffs[i];
+    int32_t meta[FK_META_WORDS] = {shift_x, shift_y, gw, gh, -1, -1, lmax, 0};
+    FK_CUDA(h, cudaMemcpyAsync(p->custom_taps, taps32.data(), (size_t)n_coeffs * sizeof(float),
+                               cudaMemcpyHostToDevice, s));
+    FK_CUDA(h, cudaMemcpyAsync(d.length, length, (size_t)n * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, s));
+    FK_CUDA(h, cudaMemcpyAsync(d.raw_length, length, (size_t)n * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, s));
+    FK_CUDA(h, cudaMemcpyAsync(d.offset, offset, (size_t)n * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, s));
+    FK_CUDA(h, cudaMemcpyAsync(d.meta, meta, sizeof meta, cudaMemcpyHostToDevice, s));
+    /* the staging vectors above are pageable: the copies have been staged on return,
+     * but synchronise anyway so `taps32` may die safely */
+    FK_CUDA(h, cudaStreamSynchronize(s));
+    p->d.taps = p->custom_taps;
+    p->custom = 1;
+    FK_CUDA(h, fk_launch_order_custom(p->d, s));
+    h->launches++;
+    p->n_frames = 1;
+    p->bound_length = lmax;
+    return FK_OK;
+}
+
+int fk_plan_read_lengths(fk_plan *p, int first, int count, int32_t *lengths_host,
+                         int32_t *meta_host, void *stream)
+{
+    if (!p) return fk_fail(nullptr, FK_EINVAL, "plan is NULL");
+    fk_handle *h = p->h;
+    if (first < 0 || count < 1 || first + count > p->n_frames)
+        return fk_fail(h, FK_EINVAL, "frames [%d, %d) outside the %d planned", first,
+                       first + count, p->n_frames);
+    FK_CUDA(h, cudaSetDevice(h->device));
+    FK_CUDA(h, cudaStreamSynchronize(as_stream(stream)));
+    if (lengths_host)
+        FK_CUDA(h, cudaMemcpy(lengths_host, p->d.length + (size_t)first * p->d.cap,
+                              (size_t)count * p->d.cap * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (meta_host)
+        FK_CUDA(h, cudaMemcpy(meta_host, p->d.meta + (size_t)first * FK_META_WORDS,
+                              (size_t)count * FK_META_WORDS * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost));
+    return FK_OK;
+}
+
+int fk_plan_read(fk_plan *p, int frame, fk_plan_view *out, void *stream)
+{
+    if (!p || !out) return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");
+    fk_handle *h = p->h;
+    if (frame < 0 || frame >= p->n_frames)
+        return fk_fail(h, FK_EINVAL, "frame %d outside the %d planned", frame, p->n_frames);
+    FK_CUDA(h, cudaSetDevice(h->device));
+    FK_CUDA(h, cudaStreamSynchronize(as_stream(stream)));
+    int32_t meta[FK_META_WORDS];
+    FK_CUDA(h, cudaMemcpy(meta, p->d.meta + (size_t)frame * FK_META_WORDS, sizeof meta,
+                          cudaMemcpyDeviceToHost));
+    out->shift_x = meta[FK_META_SX];
+    out->shift_y = meta[FK_META_SY];
+    out->grid_w = meta[FK_META_GW];
+    out->grid_h = meta[FK_META_GH];
+    out->foveal_gy = meta[FK_META_FGY];
+    out->foveal_gx = meta[FK_META_FGX];
+    out->max_length = meta[FK_META_LMAX];
+    out->status = meta[FK_META_STATUS];
+    if (out->status != 0) return FK_OK;
+    const size_t n = (size_t)out->grid_w * out->grid_h, base = (size_t)frame * p->d.cap;
+    if (out->sigma && !p->custom)
+        FK_CUDA(h, cudaMemcpy(out->sigma, p->d.sigma + base, n * sizeof(double),
+                              cudaMemcpyDeviceToHost));
+    if (out->raw_length)
+        FK_CUDA(h, cudaMemcpy(out->raw_length, p->d.raw_length + base, n * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost));
+    if (out->length)
+        FK_CUDA(h, cudaMemcpy(out->length, p->d.length + base, n * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost));
+    return FK_OK;
+}
+
+/* ----------------------------------------------------------------------- render */
+static int fk_render_any(fk_handle *h, const fk_plan *p, const void *in, void *out,
+                         int n_frames, int channels, int is_f32, void *stream)
+{
+    if (!h || !p || !in || !out) return fk_fail(h, FK_EINVAL, "NULL argument");
+    if (p->h != h) return fk_fail(h, FK_EINVAL, "plan belongs to another handle");
+    if (channels != 1 && channels != 3) /* blockwise.py:160-161 */
+        return fk_fail(h, FK_EINVAL, "render supports 1 or 3 channels, got %d", channels);
+    if (n_frames < 1 || n_frames > p->n_frames)
+        return fk_fail(h, FK_EINVAL, "n_frames %d outside the %d planned", n_frames, p->n_frames);
+    if (in == out) return fk_fail(h, FK_EINVAL, "render cannot run in place");
+    FK_CUDA(h, cudaSetDevice(h->device));
+    int launches = 0;
+    fk_plan_dev pd = p->d;
+    if (!p->custom) pd.taps = h->lut32; /* the canonical table may have grown since planning */
+    cudaError_t e = fk_launch_blur(h, pd, in, out, n_frames, channels, is_f32,
+                                   p->bound_length, as_stream(stream), &launches);
+    h->launches += launches;
+    if (e == cudaErrorInvalidConfiguration)
+        return fk_fail(h, FK_EINVAL, "filter of %d taps does not fit the device's shared memory",
+                       p->bound_length);
+    if (e != cudaSuccess) return fk_cuda_fail(h, e, "blur launch");
+    return FK_OK;
+}
+
+int fk_render_u8(fk_handle *h, const fk_plan *p, const uint8_t *in_dev, uint8_t *out_dev,
+                 int n_frames, int channels, void *stream)
+{
+    return fk_render_any(h, p, in_dev, out_dev, n_frames, channels, 0, stream);
+}
+
+int fk_render_f32(fk_handle *h, const fk_plan *p, const float *in_dev, float *out_dev,
+                  int n_frames, int channels, void *stream)
+{
+    return fk_render_any(h, p, in_dev, out_dev, n_frames, channels, 1, stream);
+}
+
+int fk_set_kernel_variant(fk_handle *h, int variant)
+{
+    if (!h) return 0;
+    int old = h->variant;
+    h->variant = variant;
+    return old;
+}
+
+int64_t fk_launch_count(const fk_handle *h) { return h ? h->launches : 0; }
+
+/* ------------------------------------------------------------ host-buffer pipeline */
+static int fk_foveate_host_any(fk_handle *h, const fk_params *prm, int W, int H, int C, int N,
+                               const double *fix, const void *in, void *out, int chunk,
+                               int is_f32)
+{
+    if (!h || !prm || !fix || !in || !out) return fk_fail(h, FK_EINVAL, "NULL argument");
+    if (C != 1 && C != 3) return fk_fail(h, FK_EINVAL, "render supports 1 or 3 channels, got %d", C);
+    if (N < 1) return fk_fail(h, FK_EINVAL, "n_frames must be >= 1");
+    if (W < 1 || H < 1) return fk_fail(h, FK_EINVAL, "image dimensions must be positive");
+    const size_t esz = is_f32 ? 4 : 1;
+    const size_t frame_bytes = (size_t)W * H * C * esz;
+    if (chunk <= 0) {
+        size_t c = ((size_t)48 << 20) / frame_bytes;
+        chunk = (int)(c < 1 ? 1 : (c > 4096 ? 4096 : c));
+    }
+    if (chunk > N) chunk = N;
+    /* keep all streams busy on small batches */
+    if (N >= fk_handle::kStreams && chunk * fk_handle::kStreams > N)
+        chunk = (N + fk_handle::kStreams - 1) / fk_handle::kStreams;
+    FK_CUDA(h, cudaSetDevice(h->device));
+    const size_t need = frame_bytes * chunk;
+    const bool replan = h->stage_w != W || h->stage_h != H ||
+                        h->stage_f != prm->fragment_size || h->stage_frames < chunk;
+    if (need > h->stage_bytes || replan) {
+        FK_CUDA(h, cudaDeviceSynchronize());
+        fk_release_stage(h);
+        for (int i = 0; i < fk_handle::kStreams; i++) {
+            FK_CUDA(h, cudaMalloc(&h->stage_in[i], need));
+            FK_CUDA(h, cudaMalloc(&h->stage_out[i], need));
+            int rc = fk_plan_create(h, W, H, prm->fragment_size, chunk, &h->stage_plan[i]);
+            if (rc != FK_OK) return rc;
+        }
+        h->stage_bytes = need;
+        h->stage_w = W;
+        h->stage_h = H;
+        h->stage_f = prm->fragment_size;
+        h->stage_frames = chunk;
+    }
+    int idx = 0;
+    for (int first = 0; first < N; first += chunk, idx++) {
+        const int n = (N - first) < chunk ? (N - first) : chunk;
+        const int slot = idx % fk_handle::kStreams;
+        cudaStream_t s = h->streams[slot];
+        const size_t off = frame_bytes * first, bytes = frame_bytes * n;
+        FK_CUDA(h, cudaMemcpyAsync(h->stage_in[slot], (const char *)in + off, bytes,
+                                   cudaMemcpyHostToDevice, s));
+        int rc = fk_plan_model(h->stage_plan[slot], prm, n, fix + 2 * (size_t)first, 0, s);
+        if (rc != FK_OK) return rc;
+        rc = fk_render_any(h, h->stage_plan[slot], h->stage_in[slot], h->stage_out[slot], n, C,
+                           is_f32, s);
+        if (rc != FK_OK) return rc;
+        FK_CUDA(h, cudaMemcpyAsync((char *)out + off, h->stage_out[slot], bytes,
+                                   cudaMemcpyDeviceToHost, s));
+    }
+    for (int i = 0; i < fk_handle::kStreams; i++) FK_CUDA(h, cudaStreamSynchronize(h->streams[i]));
+    return FK_OK;
+}
+
+int fk_foveate_host_u8(fk_handle *h, const fk_params *params, int width, int height,
+                       int channels, int n_frames, const double *fix_xy_host,
+                       const uint8_t *in_host, uint8_t *out_host, int chunk_frames)
+{
+    return fk_foveate_host_any(h, params, width, height, channels, n_frames, fix_xy_host,
+                               in_host, out_host, chunk_frames, 0);
+}
+
+int fk_foveate_host_f32(fk_handle *h, const fk_params *params, int width, int height,
+                        int channels, int n_frames, const double *fix_xy_host,
+                        const float *in_host, float *out_host, int chunk_frames)
+{
+    return fk_foveate_host_any(h, params, width, height, channels, n_frames, fix_xy_host,
+                               in_host, out_host, chunk_frames, 1);
+}
+
+int fk_host_alloc(size_t bytes, void **out)
+{
+    if (!out) return fk_fail(nullptr, FK_EINVAL, "out is NULL");
+    cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) return fk_cuda_fail(nullptr, e, "cudaHostAlloc");
+    return FK_OK;
+}
+
+int fk_host_free(void *ptr)
+{
+    if (!ptr) return FK_OK;
+    cudaError_t e = cudaFreeHost(ptr);
+    if (e != cudaSuccess) return fk_cuda_fail(nullptr, e, "cudaFreeHost");
+    return FK_OK;
+}
+
+/* --------------------------------------------------------------------- measurement */
+int fk_measure_fp32_peak(fk_handle *h, double *tflops, double *ms_out)
+{
+    if (!h || !tflops) return fk_fail(h, FK_EINVAL, "NULL argument");
+    FK_CUDA(h, cudaSetDevice(h->device));
+    const int sm = h->prop.multiProcessorCount;
+    if (!h->probe) FK_CUDA(h, cudaMalloc(&h->probe, (size_t)sm * 8 * 256 * sizeof(float)));
+    const int iters = 40000;
+    cudaEvent_t a, b;
+    FK_CUDA(h, cudaEventCreate(&a));
+    FK_CUDA(h, cudaEventCreate(&b));
+    cudaStream_t s = h->streams[0];
+    for (int i = 0; i < 3; i++) FK_CUDA(h, fk_launch_fp32_probe(h->probe, sm, iters, s));
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; rep++) {
+        FK_CUDA(h, cudaEventRecord(a, s));
+        FK_CUDA(h, fk_launch_fp32_probe(h->probe, sm, iters, s));
+        FK_CUDA(h, cudaEventRecord(b, s));
+        FK_CUDA(h, cudaEventSynchronize(b));
+        float ms = 0;
+        FK_CUDA(h, cudaEventElapsedTime(&ms, a, b));
+        best = ms < best ? ms : best;
+    }
+    h->launches += 8;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 16.0 * (double)iters * (double)sm * 8.0 * 256.0;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    if (ms_out) *ms_out = best;
+    return FK_OK;
+}
+
+} /* extern "C" */

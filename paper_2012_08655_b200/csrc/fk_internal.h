@@ -1,0 +1,102 @@
+/* fk_internal.h -- structures shared by the translation units of libfovea.so. */
+#ifndef FK_INTERNAL_H_
+#define FK_INTERNAL_H_
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/fovea.h"
+
+/* Per-frame plan header, 8 x int32 (also what fk_plan_read_lengths returns). */
+enum {
+    FK_META_SX = 0,
+    FK_META_SY = 1,
+    FK_META_GW = 2,
+    FK_META_GH = 3,
+    FK_META_FGY = 4,
+    FK_META_FGX = 5,
+    FK_META_LMAX = 6,
+    FK_META_STATUS = 7,
+    FK_META_WORDS = 8
+};
+
+#define FK_LUT_DEFAULT_MAX 255
+#define FK_PLAN_THREADS 256
+#define FK_SORT_BINS 1024 /* radius bins for the descending-cost order */
+
+/* Device-side view of a plan, passed by value to kernels. */
+struct fk_plan_dev {
+    int width, height, fragment;
+    int cap;             /* per-frame stride of the cell arrays */
+    double *sigma;       /* [frames][cap] */
+    int32_t *raw_length; /* [frames][cap] */
+    int32_t *length;     /* [frames][cap], foveal cell forced to 1 */
+    int32_t *offset;     /* [frames][cap], tap offset inside `taps` */
+    uint32_t *order;     /* [frames][cap], cell ids by descending tap count */
+    int32_t *meta;       /* [frames][FK_META_WORDS] */
+    const float *taps;   /* fp32 tap table the offsets index (canonical LUT or custom) */
+};
+
+struct fk_handle {
+    int device = -1;
+    cudaDeviceProp prop{};
+    std::string err;
+    /* canonical LUT: all odd L <= lut_max, filter L at [r*r, r*r+L) */
+    int lut_max = 0;
+    double *lut64 = nullptr;
+    float *lut32 = nullptr;
+    int variant = 0;
+    int64_t launches = 0;
+    /* pipeline resources of fk_foveate_host_* */
+    static const int kStreams = 3;
+    cudaStream_t streams[kStreams] = {nullptr, nullptr, nullptr};
+    void *stage_in[kStreams] = {nullptr, nullptr, nullptr};
+    void *stage_out[kStreams] = {nullptr, nullptr, nullptr};
+    size_t stage_bytes = 0;
+    double *stage_fix[kStreams] = {nullptr, nullptr, nullptr};
+    fk_plan *stage_plan[kStreams] = {nullptr, nullptr, nullptr};
+    int stage_w = 0, stage_h = 0, stage_f = 0, stage_frames = 0;
+    /* scratch for the FP32 peak probe */
+    float *probe = nullptr;
+};
+
+struct fk_plan {
+    fk_handle *h = nullptr;
+    int max_frames = 0;
+    int n_frames = 0;     /* frames planned by the last fk_plan_model / set_grid */
+    int bound_length = 1; /* host upper bound of the tap count over those frames */
+    int custom = 0;       /* taps point at custom_taps instead of the canonical LUT */
+    float *custom_taps = nullptr;
+    int custom_cap = 0;
+    double *fix_dev = nullptr; /* [max_frames][2] staging for host fixations */
+    fk_plan_dev d{};
+};
+
+/* error plumbing (fk_api.cu) */
+int fk_fail(fk_handle *h, int code, const char *fmt, ...);
+int fk_cuda_fail(fk_handle *h, cudaError_t e, const char *what);
+#define FK_CUDA(h, call)                                            \
+    do {                                                            \
+        cudaError_t e__ = (call);                                   \
+        if (e__ != cudaSuccess) return fk_cuda_fail((h), e__, #call); \
+    } while (0)
+
+/* kernels (fk_plan.cu, fk_blur.cu) */
+cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cudaStream_t s);
+cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
+                           const double *fix_dev, cudaStream_t s);
+cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s);
+cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
+                           int n_frames, int channels, int is_f32, int bound_length,
+                           cudaStream_t s, int *launches);
+cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s);
+
+/* Host replica of the grid geometry (tiling.py:15-28). */
+static inline int fk_span_count(int extent, int F, int offset)
+{
+    int n = extent > offset ? (extent - offset + F - 1) / F : 0;
+    return n + (offset > 0 ? 1 : 0);
+}
+
+#endif /* FK_INTERNAL_H_ */

@@ -1,0 +1,251 @@
+/*
+ * fk_plan.cu -- device-side planning for blockwise foveation (sm_100a).
+ *
+ *   fk_plan_kernel   one CTA per frame: tiling shift, grid geometry, per-fragment
+ *                    eccentricity -> sigma (fp64, bit-identical to the reference),
+ *                    tap count, foveal-fragment forcing, and a cost-descending order of
+ *                    the fragments for the render kernel.
+ *   fk_lut_kernel    Gaussian taps for every odd length (fp64 and fp32 copies).
+ *
+ * Reference arithmetic restated here (paths under /root/reference/pkg/src/foveakit/):
+ * blockwise.py:39-51, tiling.py:15-39, retinal.py:97-177, filters.py:20-38,77-85,
+ * blockwise.py:107-133.  The operation order of SURVEY.md Appendix A is kept, and every
+ * fp64 operation is an explicitly rounded intrinsic so nothing is fused.
+ */
+#include "fk_hypot.h"
+#include "fk_internal.h"
+
+namespace {
+
+__device__ __forceinline__ void fk_span(int extent, int F, int off, int g, int &a, int &b)
+{
+    /* tiling.py:21-27: starts = {0 if off > 0} U {off, off+F, ... < extent} */
+    const int lead = off > 0 ? 1 : 0;
+    if (lead && g == 0) {
+        a = 0;
+        b = off < extent ? off : extent;
+    } else {
+        a = off + (g - lead) * F;
+        b = a + F < extent ? a + F : extent;
+    }
+}
+
+__device__ __forceinline__ int fk_span_count_dev(int extent, int F, int off)
+{
+    int n = extent > off ? (extent - off + F - 1) / F : 0;
+    return n + (off > 0 ? 1 : 0);
+}
+
+/* tiling.py:36-39: searchsorted(starts, coord, side="right") - 1, clamped.
+ * starts are integers, so start <= coord  <=>  start <= floor(coord). */
+__device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, long long ic)
+{
+    int count = off > 0 ? 1 : 0;
+    if (extent > off && ic >= off) {
+        long long k = (ic - off) / F + 1;
+        int n_main = (extent - off + F - 1) / F;
+        count += (int)(k < n_main ? k : n_main);
+    }
+    int idx = count - 1;
+    idx = idx < 0 ? 0 : idx;
+    return idx > n - 1 ? n - 1 : idx;
+}
+
+/* Order the cells of frame f by descending tap count (counting sort on the radius).
+ * Called by all threads of the CTA that owns the frame; `length` must be visible. */
+__device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *hist /*BINS*/,
+                              int *scan /*blockDim.x*/)
+{
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < FK_SORT_BINS; i += nt) hist[i] = 0;
+    __syncthreads();
+    const int32_t *len = pd.length + (size_t)f * pd.cap;
+    for (int c = tid; c < ncells; c += nt) {
+        int r = (len[c] - 1) >> 1;
+        atomicAdd(&hist[r < FK_SORT_BINS ? r : FK_SORT_BINS - 1], 1);
+    }
+    __syncthreads();
+    /* suffix sums: base[b] = number of cells in bins > b.  Each thread owns a run of
+     * consecutive bins, highest first. */
+    const int per = (FK_SORT_BINS + nt - 1) / nt;
+    const int hi = FK_SORT_BINS - 1 - tid * per; /* first (highest) bin of this thread */
+    int local = 0;
+    for (int j = 0; j < per; j++) {
+        int b = hi - j;
+        if (b >= 0) local += hist[b];
+    }
+    scan[tid] = local;
+    __syncthreads();
+    if (tid == 0) { /* nt <= 256 partial sums: serial exclusive scan is a few hundred ns */
+        int run = 0;
+        for (int i = 0; i < nt; i++) {
+            int v = scan[i];
+            scan[i] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    int run = scan[tid];
+    for (int j = 0; j < per; j++) {
+        int b = hi - j;
+        if (b >= 0) {
+            int v = hist[b];
+            hist[b] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    uint32_t *order = pd.order + (size_t)f * pd.cap;
+    for (int c = tid; c < ncells; c += nt) {
+        int r = (len[c] - 1) >> 1;
+        int slot = atomicAdd(&hist[r < FK_SORT_BINS ? r : FK_SORT_BINS - 1], 1);
+        order[slot] = (uint32_t)c;
+    }
+}
+
+__global__ void __launch_bounds__(FK_PLAN_THREADS)
+fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, int n_frames)
+{
+    __shared__ int hist[FK_SORT_BINS];
+    __shared__ int scan[FK_PLAN_THREADS];
+    __shared__ int s_lmax;
+    const int f = blockIdx.x;
+    if (f >= n_frames) return;
+    const int tid = threadIdx.x;
+    const int W = pd.width, H = pd.height, F = pd.fragment;
+    const double fx = fix[2 * f], fy = fix[2 * f + 1];
+    int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
+
+    /* retinal.py:73: fixation must satisfy 0 <= fx < w and 0 <= fy < h (NaN fails) */
+    if (!(fx >= 0.0 && fx < (double)W && fy >= 0.0 && fy < (double)H)) {
+        if (tid < FK_META_WORDS) meta[tid] = tid == FK_META_STATUS ? 1 : 0;
+        return;
+    }
+    const long long ifx = (long long)floor(fx), ify = (long long)floor(fy);
+    int sx = 0, sy = 0;
+    if (prm.use_shift == 1) { /* blockwise.py:49-51, Python's non-negative modulo */
+        long long dx = (ifx - F / 2) % F, dy = (ify - F / 2) % F;
+        sx = (int)(dx < 0 ? dx + F : dx);
+        sy = (int)(dy < 0 ? dy + F : dy);
+    } else if (prm.use_shift == 2) { /* caller-chosen tiling origin (retinal.py:159-161) */
+        sx = prm.shift_x;
+        sy = prm.shift_y;
+    }
+    const int gw = fk_span_count_dev(W, F, sx), gh = fk_span_count_dev(H, F, sy);
+    const int fgx = fk_cell_of(W, F, sx, gw, ifx), fgy = fk_cell_of(H, F, sy, gh, ify);
+    const int ncells = gw * gh;
+    if (tid == 0) s_lmax = 1;
+    __syncthreads();
+
+    double *sigma = pd.sigma + (size_t)f * pd.cap;
+    int32_t *raw = pd.raw_length + (size_t)f * pd.cap;
+    int32_t *len = pd.length + (size_t)f * pd.cap;
+    int32_t *off = pd.offset + (size_t)f * pd.cap;
+    int lmax = 1;
+    for (int c = tid; c < ncells; c += blockDim.x) {
+        const int gy = c / gw, gx = c - gy * gw;
+        int x0, x1, y0, y1;
+        fk_span(W, F, sx, gx, x0, x1);
+        fk_span(H, F, sy, gy, y0, y1);
+        const double mx = __ddiv_rn((double)(x0 + x1), 2.0);          /* tiling.py:33 */
+        const double my = __ddiv_rn((double)(y0 + y1), 2.0);
+        const double d = fk_hypot(__dsub_rn(mx, fx), __dsub_rn(my, fy)); /* retinal.py:110 */
+        const double e = __dmul_rn(__ddiv_rn(d, prm.d_corner), prm.e_corner); /* :112 */
+        const double fdeg = __dmul_rn(                                  /* retinal.py:129 */
+            __ddiv_rn(prm.e2, __dmul_rn(prm.alpha, __dadd_rn(e, prm.e2))), prm.log_inv_ct0);
+        const double fpix = __ddiv_rn(__dmul_rn(0.5, fdeg), prm.fmax);  /* retinal.py:140 */
+        const double s = __ddiv_rn(prm.strength, __dmul_rn(prm.two_pi, fpix)); /* :155 */
+        sigma[c] = s;
+        /* filters.py:25-26.  Non-finite or huge sigma saturates; the host rejects such
+         * parameter sets before launching (SigmaField validation, retinal.py:93-94). */
+        double n6 = ceil(__dmul_rn(6.0, s));
+        int n = (n6 >= 1.0 && n6 < 1.0e9) ? (int)n6 : (n6 >= 1.0e9 ? 1000000001 : 1);
+        if ((n & 1) == 0) n += 1;
+        raw[c] = n;
+        const int L = (gy == fgy && gx == fgx) ? 1 : n;                 /* blockwise.py:129 */
+        len[c] = L;
+        const int r = (L - 1) >> 1;
+        off[c] = r * r;
+        lmax = L > lmax ? L : lmax;
+    }
+    atomicMax(&s_lmax, lmax);
+    __syncthreads();
+    if (tid == 0) {
+        meta[FK_META_SX] = sx;
+        meta[FK_META_SY] = sy;
+        meta[FK_META_GW] = gw;
+        meta[FK_META_GH] = gh;
+        meta[FK_META_FGY] = fgy;
+        meta[FK_META_FGX] = fgx;
+        meta[FK_META_LMAX] = s_lmax;
+        meta[FK_META_STATUS] = 0;
+    }
+    fk_sort_cells(pd, f, ncells, hist, scan);
+}
+
+/* Order pass for a caller-supplied grid (fk_plan_set_grid): frame 0 only. */
+__global__ void __launch_bounds__(FK_PLAN_THREADS) fk_order_kernel(fk_plan_dev pd)
+{
+    __shared__ int hist[FK_SORT_BINS];
+    __shared__ int scan[FK_PLAN_THREADS];
+    const int32_t *meta = pd.meta;
+    fk_sort_cells(pd, 0, meta[FK_META_GW] * meta[FK_META_GH], hist, scan);
+}
+
+/* filters.py:30-38 at sigma = L/6 (filters.py:78): one CTA per odd length. */
+__global__ void __launch_bounds__(128)
+fk_lut_kernel(double *__restrict__ lut64, float *__restrict__ lut32, int max_length)
+{
+    __shared__ double part[128];
+    const int r = blockIdx.x;
+    const int L = 2 * r + 1;
+    if (L > max_length) return;
+    const int base = r * r;
+    if (L == 1) {
+        if (threadIdx.x == 0) { lut64[0] = 1.0; lut32[0] = 1.0f; }
+        return;
+    }
+    const double sigma = __ddiv_rn((double)L, 6.0);
+    const double denom = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+    double local = 0.0;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const double k = (double)(i - r);
+        const double w = exp(-__ddiv_rn(__dmul_rn(k, k), denom));
+        lut64[base + i] = w;
+        local += w;
+    }
+    part[threadIdx.x] = local;
+    __syncthreads();
+    for (int s = 64; s > 0; s >>= 1) {
+        if (threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double sum = part[0];
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const double w = __ddiv_rn(lut64[base + i], sum);
+        lut64[base + i] = w;
+        lut32[base + i] = (float)w;
+    }
+}
+
+} // namespace
+
+cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cudaStream_t s)
+{
+    const int nr = (max_length - 1) / 2 + 1;
+    fk_lut_kernel<<<nr, 128, 0, s>>>(lut64, lut32, max_length);
+    return cudaGetLastError();
+}
+
+cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
+                           const double *fix_dev, cudaStream_t s)
+{
+    fk_plan_kernel<<<n_frames, FK_PLAN_THREADS, 0, s>>>(pd, prm, fix_dev, n_frames);
+    return cudaGetLastError();
+}
+
+cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s)
+{
+    fk_order_kernel<<<1, FK_PLAN_THREADS, 0, s>>>(pd);
+    return cudaGetLastError();
+}

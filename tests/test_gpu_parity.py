@@ -1,0 +1,405 @@
+"""Parity of the CUDA path (through the C ABI) with the reference: golden vectors made by
+the reference itself, the CPU oracle on the same seeded inputs, and size-independent
+properties at the BASELINE.json sizes.  Bars (BASELINE.json north_star): sigma / tap
+counts / index grid / shift / foveal cell bit-exact; uint8 output max-abs <= 1 with
+identity fragments byte-exact; float32 output within 1e-4 relative."""
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+from cases import (BIG_RENDER_CASES, F32_CASES, PLAN_CASES, RENDER_CASES,  # noqa: E402
+                   frame_f32, frame_u8)
+
+import paper_2012_08655_b200 as fk  # noqa: E402
+from oracle import fovea_oracle as fo  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+U8_TOL = 1          # north_star: max-abs error <= 1/255 on uint8 output
+F32_RTOL = 1e-4     # north_star: <= 1e-4 relative on fp32 output
+
+
+def maxdiff(a, b):
+    return int(np.abs(a.astype(np.int16) - b.astype(np.int16)).max())
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+# ----------------------------------------------------------------------------- plan
+@pytest.mark.parametrize("case", PLAN_CASES, ids=[c[0] for c in PLAN_CASES])
+def test_plan_matches_reference_golden(golden, case):
+    name, size, kw, use_shift = case
+    g = golden["plans"]
+    p = fk.FoveationParams(**kw)
+    grid, bank = fk.plan(size, p, use_shift=use_shift)
+    assert tuple(grid.shift) == tuple(int(v) for v in g[f"{name}/shift"])
+    assert tuple(grid.foveal_cell) == tuple(int(v) for v in g[f"{name}/foveal"])
+    assert np.array_equal(grid.index, g[f"{name}/index"])
+    assert np.array_equal(bank.lengths, g[f"{name}/bank_lengths"])
+    assert grid.region_count() == int(g[f"{name}/regions"])
+    field = fk.build_sigma_field(size, p, grid.shift)
+    assert field.sigma.shape == g[f"{name}/sigma"].shape
+    assert np.array_equal(bits(field.sigma), bits(g[f"{name}/sigma"])), "sigma not bit-exact"
+    assert np.array_equal(fk.filter_length(field.sigma), g[f"{name}/raw_length"])
+
+
+def test_plan_batch_random_vs_oracle():
+    """Random geometries and fractional fixations, planned as batches on the device."""
+    rng = np.random.default_rng(2024)
+    eng = fk.get_engine(0)
+    for trial in range(40):
+        F = int(rng.choice([4, 8, 12, 16, 32, 64, 100]))
+        w, h = int(rng.integers(1, 700)), int(rng.integers(1, 500))
+        kw = dict(fragment_size=F, e2=float(rng.uniform(0.8, 4)), alpha=float(rng.uniform(0.05, 0.3)),
+                  ct0=float(rng.uniform(0.005, 0.1)), e_corner=float(rng.uniform(0, 90)),
+                  strength=float(rng.uniform(0, 2.5)))
+        if trial % 3 == 0:
+            kw["f_max"] = float(rng.uniform(10, 60))
+        n = 16
+        fix = np.stack([rng.uniform(0, w, n), rng.uniform(0, h, n)], axis=1)
+        fix[::4] = np.floor(fix[::4])          # integer-pixel fixations too
+        fix[1] = (0.0, 0.0)
+        fix[2] = (np.nextafter(float(w), 0.0), np.nextafter(float(h), 0.0))
+        p = fk.FoveationParams(**kw)
+        plan = eng.plan_for((w, h), F, n)
+        plan.model(p, fix, use_shift=(trial % 5 != 0))
+        for i in range(n):
+            got = plan.read(i)
+            ref = fo.c_plan((w, h), fo.OracleParams(fixation=tuple(fix[i]), **kw),
+                            use_shift=(trial % 5 != 0))
+            assert got["shift"] == ref["shift"]
+            assert got["foveal"] == ref["foveal"]
+            assert got["sigma"].shape == ref["sigma"].shape
+            assert np.array_equal(bits(got["sigma"]), bits(ref["sigma"]))
+            assert np.array_equal(got["raw_length"], ref["raw_length"])
+            assert np.array_equal(got["length"], ref["length"])
+            assert got["max_length"] == int(ref["length"].max())
+
+
+def test_plan_order_is_a_cost_descending_permutation():
+    eng = fk.get_engine(0)
+    plan = eng.plan_for((1920, 1080), 32, 4)
+    fix = np.asarray([[960, 540], [0, 0], [1919, 1079], [300.5, 700.25]], dtype=np.float64)
+    plan.model(fk.FoveationParams(), fix)
+    lengths, meta = plan.read_lengths()
+    assert meta.shape == (4, 8) and np.all(meta[:, 7] == 0)
+    for i in range(4):
+        gw, gh = meta[i, 2], meta[i, 3]
+        assert lengths[i, : gw * gh].max() == meta[i, 6]
+        assert lengths[i, meta[i, 4] * gw + meta[i, 5]] == 1   # foveal cell forced
+
+
+def test_lut_taps_match_reference(golden):
+    g = golden["taps"]
+    eng = fk.get_engine(0)
+    for key in g.files:
+        L = int(key[1:])
+        taps = eng.lut_taps(L)
+        assert taps.shape == g[key].shape
+        assert np.max(np.abs(taps - g[key])) <= 1e-12
+        assert abs(taps.sum() - 1.0) <= 1e-9
+        assert np.allclose(taps, taps[::-1], rtol=0, atol=1e-15)
+
+
+def test_bank_from_sigmas_kat():
+    # test_filters.py:105-128: lengths [1,3,7,31], index [1,2,2,3], cumulative [1,4,11,42]
+    field = fk.SigmaField(grid_width=4, grid_height=1,
+                          sigma=np.asarray([[0.2, 1.0, 1.1, 5.0]]))
+    bank, index = fk.build_bank(field)
+    assert list(bank.lengths) == [1, 3, 7, 31]
+    assert list(index[0]) == [1, 2, 2, 3]
+    assert list(bank.cumulative_sizes) == [1, 4, 11, 42]
+    assert fk.total_coefficients(bank) == 42
+
+
+# --------------------------------------------------------------------------- render
+@pytest.mark.parametrize("case", RENDER_CASES, ids=[c[0] for c in RENDER_CASES])
+def test_render_u8_matches_reference_golden(golden, case):
+    name, seed, shape, kw = case
+    ref = golden["renders_u8"][f"{name}/out"]
+    stats_ref = golden["renders_u8"][f"{name}/stats"]
+    img = frame_u8(seed, shape)
+    out, grid, bank, stats = fk.foveate(fk.RasterImage.from_array(img), fk.FoveationParams(**kw))
+    assert out.data.shape == ref.shape and out.data.dtype == np.uint8
+    assert maxdiff(out.data, ref) <= U8_TOL
+    assert (out.data != ref).mean() < 2e-3          # only .5 ties may flip
+    assert [stats.regions, stats.max_filter, *stats.shift] == [int(v) for v in stats_ref]
+
+
+@pytest.mark.parametrize("case", BIG_RENDER_CASES, ids=[c[0] for c in BIG_RENDER_CASES])
+def test_render_1080p_matches_reference_and_oracle(golden, case):
+    name, seed, shape, kw = case
+    g = golden["renders_big"]
+    img = frame_u8(seed, shape)
+    out, grid, bank, stats = fk.foveate(fk.RasterImage.from_array(img), fk.FoveationParams(**kw))
+    assert maxdiff(out.data[::7, ::11], g[f"{name}/sample"]) <= U8_TOL
+    assert [stats.regions, stats.max_filter, *stats.shift] == [int(v) for v in g[f"{name}/stats"]]
+    ref, pl = fo.c_foveate(img, fo.OracleParams(**kw), threads=8)
+    assert maxdiff(out.data, ref) <= U8_TOL
+    assert (out.data != ref).mean() < 2e-3
+    # identity fragments (the foveal cell) are byte-exact
+    sx = fk.fragment_spans(shape[1], 32, grid.shift[0])
+    sy = fk.fragment_spans(shape[0], 32, grid.shift[1])
+    gy, gx = grid.foveal_cell
+    sl = np.s_[sy[gy, 0]:sy[gy, 1], sx[gx, 0]:sx[gx, 1]]
+    assert np.array_equal(out.data[sl], img[sl])
+
+
+@pytest.mark.parametrize("case", F32_CASES, ids=[c[0] for c in F32_CASES])
+def test_render_f32_matches_reference_golden(golden, case):
+    name, seed, shape, kw = case
+    ref = golden["renders_f32"][f"{name}/out"]
+    img = frame_f32(seed, shape)
+    p = fk.FoveationParams(**kw)
+    fix = np.asarray([p.fixation_for((shape[1], shape[0]))])
+    out = fk.foveate_batch(torch.from_numpy(img)[None].cuda(), fix, p)[0].cpu().numpy()
+    assert out.dtype == np.float32
+    err = np.abs(out.astype(np.float64) - ref)
+    assert np.all(err <= F32_RTOL * np.maximum(np.abs(ref), 1.0))
+
+
+@pytest.mark.parametrize("L", [7, 13, 31])
+def test_uniform_grid_matches_reference(golden, L):
+    # test_blockwise.py:135-148: one bank filter everywhere, no shift
+    ref = golden["renders_uniform"][f"L{L}/out"]
+    img = np.random.default_rng(L).integers(0, 256, (128, 128, 3)).astype(np.uint8)
+    field = fk.SigmaField(grid_width=1, grid_height=1, sigma=np.asarray([[L / 6.0]]))
+    bank = fk.build_bank(field)[0]
+    assert bank.lengths[1] == L
+    grid = fk.BlurGrid(index=np.full((4, 4), 1, np.int64), shift=(0, 0), fragment_size=32,
+                       foveal_cell=(0, 0))
+    out = fk.render(fk.RasterImage.from_array(img), grid, bank)
+    assert maxdiff(out.data, ref) <= U8_TOL
+
+
+def test_render_accepts_arbitrary_bank_taps():
+    """render() honours the bank's own coefficients, not only the canonical LUT."""
+    img = frame_u8(3, (64, 96, 3))
+    box = np.full(5, 0.2)
+    bank = fk.FilterBank(filters=(np.array([1.0]), box), lengths=np.array([1, 5]),
+                         cumulative_sizes=np.array([1, 6]), sigmas=np.array([1 / 6, 5 / 6]))
+    idx = np.ones((4, 6), np.int64)
+    idx[1, 2] = 0
+    grid = fk.BlurGrid(index=idx, shift=(0, 0), fragment_size=16, foveal_cell=(1, 2))
+    out = fk.render(fk.RasterImage.from_array(img), grid, bank)
+    lengths = np.where(idx == 1, 5, 1)
+    ref = fo.c_render(img, 16, (0, 0), lengths, coeffs=np.concatenate(([1.0], box)),
+                      offsets=np.where(idx == 1, 1, 0))
+    assert maxdiff(out.data, ref) <= U8_TOL
+    assert np.array_equal(out.data[16:32, 32:48], img[16:32, 32:48])
+
+
+# ----------------------------------------------------------------------- properties
+def test_constant_and_identity_images():
+    # test_blockwise.py:121-133
+    const = fk.RasterImage.from_array(np.full((1080, 1920, 3), 128, np.uint8))
+    out, *_ = fk.foveate(const, fk.FoveationParams(fixation=(0, 0)))
+    assert out == const
+    img = fk.RasterImage.from_array(frame_u8(5, (1080, 1920, 3)))
+    out, grid, bank, stats = fk.foveate(img, fk.FoveationParams(strength=0.0))
+    assert out == img and stats.regions == 1 and len(bank) == 1   # test_blockwise.py:190-194
+    for v in (0, 255):
+        flat = fk.RasterImage.from_array(np.full((96, 160, 3), v, np.uint8))
+        assert fk.foveate(flat, fk.FoveationParams(fragment_size=16))[0] == flat
+
+
+def test_determinism_and_fragment_independence():
+    # test_blockwise.py:150-173
+    img = frame_u8(11, (96, 96, 3))
+    field = fk.SigmaField(grid_width=1, grid_height=1, sigma=np.asarray([[2.0]]))
+    bank = fk.build_bank(field)[0]                  # 13 taps, radius 6
+    grid = fk.BlurGrid(index=np.ones((3, 3), np.int64), shift=(0, 0), fragment_size=32,
+                       foveal_cell=(0, 0))
+    a = fk.render(fk.RasterImage.from_array(img), grid, bank, workers=1)
+    b = fk.render(fk.RasterImage.from_array(img), grid, bank, workers=8)
+    assert np.array_equal(a.data, b.data)
+    pert = img.copy()
+    pert[60:, 60:, :] = frame_u8(12, (36, 36, 3))
+    c = fk.render(fk.RasterImage.from_array(pert), grid, bank)
+    assert np.array_equal(a.data[:32, :32], c.data[:32, :32])
+
+
+def test_foveal_passthrough_and_single_channel():
+    # test_acceptance.py:135-148 configurations; test_blockwise.py:182-186,196-204
+    for F, fix, seed in ((16, (256, 256), 1), (32, (37, 411), 2), (8, (500, 3), 3)):
+        img = frame_u8(seed, (512, 512, 3))
+        out, grid, _, _ = fk.foveate(fk.RasterImage.from_array(img),
+                                     fk.FoveationParams(fragment_size=F, fixation=fix))
+        sx = fk.fragment_spans(512, F, grid.shift[0])
+        sy = fk.fragment_spans(512, F, grid.shift[1])
+        gy, gx = grid.foveal_cell
+        sl = np.s_[sy[gy, 0]:sy[gy, 1], sx[gx, 0]:sx[gx, 1]]
+        assert np.array_equal(out.data[sl], img[sl])
+        assert grid.index[grid.foveal_cell] == 0
+    gray = frame_u8(2, (64, 64, 1))
+    out, *_ = fk.foveate(fk.RasterImage.from_array(gray), fk.FoveationParams(fragment_size=16))
+    assert out.channels == 1 and out.size == (64, 64)
+    ref, _ = fo.c_foveate(gray, fo.OracleParams(fragment_size=16))
+    assert maxdiff(out.data, ref) <= U8_TOL
+
+
+def test_mean_preserved_and_tv_not_increased():
+    # test_blockwise.py:206-232 on a smooth synthetic scene
+    yy, xx = np.mgrid[0:512, 0:512]
+    rng = np.random.default_rng(0)
+    scene = 128 + 60 * np.sin(xx / 9.0) * np.cos(yy / 13.0) + rng.normal(0, 12, (512, 512))
+    img = np.clip(np.stack([scene, scene[::-1], scene[:, ::-1]], axis=2), 0, 255).astype(np.uint8)
+    out, grid, bank, _ = fk.foveate(fk.RasterImage.from_array(img),
+                                    fk.FoveationParams(fragment_size=16))
+    assert abs(float(out.data.mean()) - float(img.mean())) <= 1.0
+
+    def tv(a):
+        a = a.astype(np.int64)
+        return np.abs(np.diff(a, axis=0)).sum() + np.abs(np.diff(a, axis=1)).sum()
+
+    sx = fk.fragment_spans(512, 16, grid.shift[0])
+    sy = fk.fragment_spans(512, 16, grid.shift[1])
+    for gy in range(0, grid.index.shape[0], 3):
+        for gx in range(0, grid.index.shape[1], 3):
+            if bank.lengths[grid.index[gy, gx]] < 3:
+                continue
+            sl = np.s_[sy[gy, 0]:sy[gy, 1], sx[gx, 0]:sx[gx, 1]]
+            fo_, fi_ = out.data[sl], img[sl]
+            hh, ww = fo_.shape[:2]
+            assert tv(fo_) <= tv(fi_) + ((hh - 1) * ww + hh * (ww - 1)) * 3
+
+
+def test_error_behaviour_matches_reference():
+    img = fk.RasterImage.from_array(np.zeros((32, 32, 3), np.uint8))
+    bank = fk.build_bank(fk.SigmaField(1, 1, np.asarray([[0.0]])))[0]
+    grid = fk.BlurGrid(index=np.full((2, 2), 3, np.int64), shift=(0, 0), fragment_size=16,
+                       foveal_cell=(0, 0))
+    with pytest.raises(ValueError, match="bank"):            # test_blockwise.py:175-180
+        fk.render(img, grid, bank)
+    bad = fk.BlurGrid(index=np.zeros((3, 2), np.int64), shift=(0, 0), fragment_size=16,
+                      foveal_cell=(0, 0))
+    with pytest.raises(ValueError, match="does not match image"):
+        fk.render(img, bad, bank)
+    p = fk.FoveationParams(fragment_size=16, fixation=(64, 64))
+    shift = fk.compute_fragment_shift((64, 64), 16)
+    field = fk.build_sigma_field((128, 128), p, shift)
+    bnk, index = fk.build_bank(field)
+    with pytest.raises(ValueError, match="tiling"):          # test_blockwise.py:94-100
+        fk.build_blur_grid(field, bnk, index, (64, 64), (256, 256), 16, shift)
+    with pytest.raises(ValueError, match="outside"):
+        fk.plan((100, 100), fk.FoveationParams(fixation=(100, 5)))
+    with pytest.raises(ValueError, match="sigma_max"):       # test_blockwise.py:234-237
+        fk.foveate(img, fk.FoveationParams(fragment_size=16),
+                   density=fk.RasterImage.from_array(np.zeros((8, 8), np.uint8)))
+    with pytest.raises(ValueError, match="outside"):
+        fk.foveate_batch(np.zeros((2, 32, 32, 3), np.uint8), [[5, 5], [40, 1]])
+    # the C ABI itself rejects what the shim would (no shim-only validation)
+    eng = fk.get_engine(0)
+    plan = eng.plan_for((32, 32), 16, 1)
+    with pytest.raises(ValueError, match="outside"):
+        plan.model(fk.FoveationParams(fragment_size=16), [[32.0, 0.0]])
+    with pytest.raises(ValueError, match="channels"):
+        plan.model(fk.FoveationParams(fragment_size=16), [[3.0, 3.0]])
+        eng.render(torch.zeros((1, 32, 32, 2), dtype=torch.uint8, device="cuda"), plan)
+
+
+def test_zero_strength_grid_and_symmetry():
+    # test_blockwise.py:73-87
+    grid, bank = fk.plan((128, 128), fk.FoveationParams(strength=0.0, fragment_size=16,
+                                                        fixation=(64, 64)))
+    assert np.all(grid.index == 0) and len(bank) == 1
+    grid, _ = fk.plan((256, 256), fk.FoveationParams(fragment_size=16, fixation=(128.0, 128.0)))
+    assert np.array_equal(grid.index, grid.index[::-1, ::-1])
+    f = fk.build_sigma_field((256, 256), fk.FoveationParams(fragment_size=16,
+                                                            fixation=(128.0, 128.0)), (8, 8))
+    assert np.array_equal(f.sigma, f.sigma[::-1, :]) and np.array_equal(f.sigma, f.sigma[:, ::-1])
+
+
+# ---------------------------------------------------------------------------- batch
+def moving_fixations(n, w=1920, h=1080):
+    i = np.arange(n)
+    return np.stack([np.floor(w / 2 + 0.4 * w * np.cos(2 * np.pi * i / n)),
+                     np.floor(h / 2 + 0.4 * h * np.sin(2 * np.pi * i / n))], axis=1)
+
+
+def test_batch_1080p_moving_fixation_vs_oracle():
+    """BASELINE config 2 shape (fewer frames): per-frame fixations, device tensors."""
+    n = 6
+    frames = frame_u8(0, (n, 1080, 1920, 3))
+    fix = moving_fixations(n)
+    out = fk.foveate_batch(torch.from_numpy(frames).cuda(), fix, fk.FoveationParams())
+    out = out.cpu().numpy()
+    for i in range(n):
+        ref, _ = fo.c_foveate(frames[i], fo.OracleParams(fixation=tuple(fix[i])), threads=8)
+        assert maxdiff(out[i], ref) <= U8_TOL
+        assert (out[i] != ref).mean() < 2e-3
+
+
+def test_host_pipeline_equals_device_path_and_shards():
+    n = 20
+    frames = frame_u8(7, (n, 270, 480, 3))
+    fix = np.random.default_rng(7).uniform(0, 1, (n, 2)) * [480, 270]
+    p = fk.FoveationParams(fragment_size=16)
+    dev = fk.foveate_batch(torch.from_numpy(frames).cuda(), fix, p).cpu().numpy()
+    host = fk.foveate_batch(frames, fix, p, chunk_frames=3)
+    assert np.array_equal(dev, host)
+    pinned_in = fk.pinned_empty(frames.shape, np.uint8)
+    pinned_in[...] = frames
+    pinned_out = fk.pinned_empty(frames.shape, np.uint8)
+    got = fk.foveate_batch(pinned_in, fix, p, out=pinned_out)
+    assert got is pinned_out and np.array_equal(pinned_out, dev)
+    # sharding over a device list (the same GPU twice exercises the split/merge logic)
+    sharded = fk.foveate_batch(frames, fix, p, devices=[0, 0])
+    assert np.array_equal(sharded, dev)
+    ref, _ = fo.c_foveate(frames[5], fo.OracleParams(fragment_size=16, fixation=tuple(fix[5])))
+    assert maxdiff(dev[5], ref) <= U8_TOL
+
+
+def test_batch_256x256_random_fixations_vs_oracle():
+    """BASELINE config 4 shape (subset): many small frames, random fixations."""
+    n = 512
+    rng = np.random.default_rng(1)
+    frames = rng.integers(0, 256, (n, 256, 256, 3), dtype=np.uint8)
+    fix = rng.integers(0, 256, (n, 2)).astype(np.float64)
+    out = fk.foveate_batch(torch.from_numpy(frames).cuda(), fix, fk.FoveationParams()).cpu().numpy()
+    for i in range(0, n, 37):
+        ref, _ = fo.c_foveate(frames[i], fo.OracleParams(fixation=tuple(fix[i])), threads=8)
+        assert maxdiff(out[i], ref) <= U8_TOL
+
+
+def test_4k_f16_vs_oracle():
+    """BASELINE config 3: 3840x2160, 16x16 fragments, corner fixation (largest halos)."""
+    img = frame_u8(3, (2160, 3840, 3))
+    kw = dict(fragment_size=16, fixation=(0, 0))
+    out, grid, bank, stats = fk.foveate(fk.RasterImage.from_array(img), fk.FoveationParams(**kw))
+    assert stats.max_filter == 103 and grid.index.shape == (136, 241)
+    ref, _ = fo.c_foveate(img, fo.OracleParams(**kw), threads=8)
+    assert maxdiff(out.data, ref) <= U8_TOL
+    assert (out.data != ref).mean() < 2e-3
+
+
+@pytest.mark.parametrize("F", [8, 16, 32, 64])
+def test_f32_block_size_sweep_alt_fit_vs_oracle(F):
+    """BASELINE config 5: fp32 frames, steeper fit (e2=1.5), block sizes 8..64."""
+    img = frame_f32(50 + F, (540, 960, 3))
+    kw = dict(fragment_size=F, e2=1.5)
+    p = fk.FoveationParams(**kw)
+    out = fk.foveate_batch(torch.from_numpy(img)[None].cuda(), None, p)[0].cpu().numpy()
+    ref, _ = fo.c_foveate(img, fo.OracleParams(**kw), quantize=False, threads=8)
+    err = np.abs(out.astype(np.float64) - ref)
+    assert np.all(err <= F32_RTOL * np.maximum(np.abs(ref), 1.0))
+    # linearity of the fp32 path: foveate(a*x + b) == a*foveate(x) + b within tolerance
+    out2 = fk.foveate_batch(torch.from_numpy(0.5 * img + 0.25)[None].cuda(), None, p)[0].cpu().numpy()
+    assert np.allclose(out2, 0.5 * out + 0.25, rtol=0, atol=2e-5)
+
+
+def test_long_filters_grow_the_lut_and_strip_path():
+    """strength 6 -> filters of several hundred taps (beyond the default 255-tap LUT)."""
+    img = frame_u8(9, (120, 200, 3))
+    kw = dict(fragment_size=32, fixation=(10, 10), strength=6.0)
+    out, grid, bank, stats = fk.foveate(fk.RasterImage.from_array(img), fk.FoveationParams(**kw))
+    assert stats.max_filter > 255
+    ref, _ = fo.c_foveate(img, fo.OracleParams(**kw), threads=8)
+    assert maxdiff(out.data, ref) <= U8_TOL
