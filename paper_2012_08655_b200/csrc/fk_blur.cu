@@ -161,6 +161,16 @@ cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, 
                            int n_frames, int channels, int is_f32, int bound_length,
                            cudaStream_t s, int *launches)
 {
+    if (h->variant != 1) { /* fast path unless the generic kernel is forced */
+        bool taken = false;
+        cudaError_t fe = fk_launch_blur_fast(h, pd, in, out, n_frames, channels, is_f32,
+                                             bound_length, s, &taken);
+        if (fe != cudaSuccess) return fe;
+        if (taken) {
+            *launches += 1;
+            return cudaSuccess;
+        }
+    }
     const int F = pd.fragment;
     const int r = (bound_length - 1) / 2;
     const int w_floats = (bound_length + 3) & ~3;

@@ -1,0 +1,349 @@
+/*
+ * fk_blur_fast.cu -- register-blocked separable blur for sm_100a (the hot kernel).
+ *
+ * Same arithmetic as blockwise.py:136-153 (_render_cell): clamp-to-edge tile, horizontal
+ * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
+ * (convolve.py:15).  What differs from fk_blur_generic is only how the work is laid out:
+ *
+ *   work item   one <=32x32 sub-rectangle of a fragment (all of it for F <= 32), one CTA
+ *               of 128 threads per item, items ordered by descending tap count per frame.
+ *   staging     the tile is converted to fp32 once and staged in shared memory in blocks
+ *               of 32 tile rows; row pitch = 4 (mod 8) floats so LDS.128 from 8 different
+ *               rows hits 8 different bank groups.
+ *   H pass      one task = 8 pixels x C channels of one tile row (8C accumulators).  The
+ *               taps are walked in chunks of 4; the input window lives in 12C registers
+ *               used as a ring with compile-time indices, refilled with LDS.128 as soon
+ *               as a quad of values is dead, so the inner loop is 32C FFMA per
+ *               (C + 1) LDS.128 -- the FP32 pipe, not the LSU, is the limiter.
+ *   V pass      one task = 8 output rows x 4 adjacent floats, same ring scheme over rows
+ *               of the intermediate (128 FFMA per 5 LDS.128).
+ *
+ * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can
+ * touch is zero-filled so 0 * garbage never produces a NaN.
+ */
+#include "fk_internal.h"
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kTB = 32;   /* tile rows staged per block */
+constexpr int kRV = 8;    /* output rows per V task */
+constexpr int kSub = 32;  /* sub-rectangle edge */
+constexpr int kNQ = 6;    /* tile columns a thread may own while staging (kNQ * 128 floats) */
+
+template <typename T> struct fast_px;
+template <> struct fast_px<uint8_t> {
+    static __device__ __forceinline__ float load(const uint8_t *p) { return (float)__ldg(p); }
+    static __device__ __forceinline__ uint8_t store(float v)
+    {
+        v = floorf(v + 0.5f); /* convolve.py:15 */
+        v = fminf(fmaxf(v, 0.0f), 255.0f);
+        return (uint8_t)v;
+    }
+};
+template <> struct fast_px<float> {
+    static __device__ __forceinline__ float load(const float *p) { return __ldg(p); }
+    static __device__ __forceinline__ float store(float v) { return v; }
+};
+
+__device__ __forceinline__ void fast_span(int extent, int F, int off, int g, int &a, int &b)
+{
+    const int lead = off > 0 ? 1 : 0;
+    if (lead && g == 0) {
+        a = 0;
+        b = off < extent ? off : extent;
+    } else {
+        a = off + (g - lead) * F;
+        b = a + F < extent ? a + F : extent;
+    }
+}
+
+__device__ __forceinline__ int fast_clamp(int v, int lo, int hi)
+{
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+
+/*
+ * Horizontal task: out[j] = sum_k g[k] * in[j + C*k], j in [0, 8C), for one tile row.
+ * `trow` points at the first input float of the segment (16-byte aligned), `wts` at the
+ * zero-padded taps, nchunk = ceil(L / 4).
+ */
+template <int C>
+__device__ __forceinline__ void h_task(const float *__restrict__ trow,
+                                       const float *__restrict__ wts, int nchunk,
+                                       float *__restrict__ irow)
+{
+    constexpr int NW = 12 * C; /* ring of input values */
+    constexpr int NA = 8 * C;  /* accumulators */
+    float win[NW];
+    float acc[NA];
+#pragma unroll
+    for (int j = 0; j < NA; j++) acc[j] = 0.0f;
+    const float4 *src = reinterpret_cast<const float4 *>(trow);
+#pragma unroll
+    for (int v = 0; v < NW / 4; v++) {
+        const float4 x = src[v];
+        win[4 * v + 0] = x.x;
+        win[4 * v + 1] = x.y;
+        win[4 * v + 2] = x.z;
+        win[4 * v + 3] = x.w;
+    }
+    const float4 *nxt = src + NW / 4;
+    const float4 *wp = reinterpret_cast<const float4 *>(wts);
+    for (int c = 0; c < nchunk; c += 3) {
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            if (p > 0 && c + p >= nchunk) break;
+            const float4 g4 = wp[c + p];
+            const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+#pragma unroll
+                for (int j = 0; j < NA; j++)
+                    acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
+                /* values below C*(t+1) of this chunk are dead: refill whole quads */
+#pragma unroll
+                for (int v = 0; v < C; v++) {
+                    if (4 * (v + 1) <= C * (t + 1) && 4 * (v + 1) > C * t) {
+                        const float4 x = nxt[v];
+                        const int q = ((p * C + v) % (3 * C)) * 4;
+                        win[q + 0] = x.x;
+                        win[q + 1] = x.y;
+                        win[q + 2] = x.z;
+                        win[q + 3] = x.w;
+                    }
+                }
+            }
+            nxt += C;
+        }
+    }
+    float4 *dst = reinterpret_cast<float4 *>(irow);
+#pragma unroll
+    for (int v = 0; v < NA / 4; v++)
+        dst[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+}
+
+/*
+ * Vertical task: acc[j][i] = sum_k g[k] * I[row0 + j + k][col0 + i], j < 8, i < 4.
+ * `icol` points at I[row0][col0]; pitch in floats.
+ */
+__device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch,
+                                       const float *__restrict__ wts, int nchunk,
+                                       float (&acc)[kRV][4])
+{
+    float4 win[12];
+#pragma unroll
+    for (int j = 0; j < kRV; j++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) acc[j][i] = 0.0f;
+#pragma unroll
+    for (int v = 0; v < 12; v++)
+        win[v] = *reinterpret_cast<const float4 *>(icol + (size_t)v * pitch);
+    const float *nxt = icol + (size_t)12 * pitch;
+    const float4 *wp = reinterpret_cast<const float4 *>(wts);
+    for (int c = 0; c < nchunk; c += 3) {
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            if (p > 0 && c + p >= nchunk) break;
+            const float4 g4 = wp[c + p];
+            const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+#pragma unroll
+                for (int j = 0; j < kRV; j++) {
+                    const float4 x = win[(4 * p + t + j) % 12];
+                    acc[j][0] = fmaf(g[t], x.x, acc[j][0]);
+                    acc[j][1] = fmaf(g[t], x.y, acc[j][1]);
+                    acc[j][2] = fmaf(g[t], x.z, acc[j][2]);
+                    acc[j][3] = fmaf(g[t], x.w, acc[j][3]);
+                }
+                /* row t of this chunk is dead: refill its slot with the row 12 ahead */
+                win[(4 * p + t) % 12] =
+                    *reinterpret_cast<const float4 *>(nxt + (size_t)t * pitch);
+            }
+            nxt += (size_t)4 * pitch;
+        }
+    }
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(kThreads, 4)
+fk_blur_fast(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int n_frames,
+             int nsub, int wts_floats, int twp, int irows)
+{
+    constexpr int SEG = 8 * C;
+    constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
+    constexpr int IWP = NSEG_MAX * SEG + 4;               /* pitch/4 odd: 100 or 36 */
+    extern __shared__ __align__(16) float smem[];
+    float *wts = smem;
+    float *tile = wts + wts_floats;
+    float *interm = tile + kTB * twp;
+
+    /* ---- decode the work item ------------------------------------------------ */
+    const int nsub2 = nsub * nsub;
+    const unsigned item = blockIdx.x / nsub2;
+    const int sub = blockIdx.x - item * nsub2;
+    const int f = item / pd.cap;
+    const int slot = item - f * pd.cap;
+    if (f >= n_frames) return;
+    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
+    if (meta[FK_META_STATUS] != 0) return;
+    const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
+    if (slot >= gw * gh) return;
+    const int cell = (int)pd.order[(size_t)f * pd.cap + slot];
+    const int gy = cell / gw, gx = cell - gy * gw;
+    const int W = pd.width, H = pd.height;
+    int cx0, cx1, cy0, cy1;
+    fast_span(W, pd.fragment, meta[FK_META_SX], gx, cx0, cx1);
+    fast_span(H, pd.fragment, meta[FK_META_SY], gy, cy0, cy1);
+    const int sby = sub / nsub, sbx = sub - sby * nsub;
+    const int x0 = cx0 + sbx * kSub, y0 = cy0 + sby * kSub;
+    if (x0 >= cx1 || y0 >= cy1) return;
+    const int x1 = x0 + kSub < cx1 ? x0 + kSub : cx1;
+    const int y1 = y0 + kSub < cy1 ? y0 + kSub : cy1;
+    const int fw = x1 - x0, fh = y1 - y0;
+    const int L = pd.length[(size_t)f * pd.cap + cell];
+    const size_t frame_off = (size_t)f * H * W * C;
+    const T *src = in + frame_off;
+    T *dst = out + frame_off;
+    const int tid = threadIdx.x;
+
+    if (L == 1) { /* blockwise.py:141-143 */
+        const int rowlen = fw * C;
+        for (int i = tid; i < fh * rowlen; i += kThreads) {
+            const int y = i / rowlen, c = i - y * rowlen;
+            const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
+            dst[o] = src[o];
+        }
+        return;
+    }
+    const int r = (L - 1) >> 1;
+    const int nchunk = (L + 3) >> 2;
+    const int th = fh + 2 * r;
+    const int nseg = (fw * C + SEG - 1) / SEG;
+    const int tw = (fw + 2 * r) * C;                    /* valid tile floats per row */
+    const int twz = C * (8 * nseg + 4 + 4 * nchunk);    /* floats the H tasks may touch */
+
+    {   /* taps, zero-padded; zero rows of the intermediate that padded taps may touch */
+        const float *taps = pd.taps + pd.offset[(size_t)f * pd.cap + cell];
+        for (int i = tid; i < 4 * nchunk; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
+        const int rows_touched = ((fh + kRV - 1) / kRV) * kRV + 4 + 4 * nchunk;
+        float4 *z = reinterpret_cast<float4 *>(interm + (size_t)th * IWP);
+        const int nz = (rows_touched - th) * (IWP / 4);
+        for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+
+    /* ---- staging ownership: each thread owns up to kNQ tile columns ------------ */
+    int coff[kNQ];
+#pragma unroll
+    for (int q = 0; q < kNQ; q++) {
+        const int j = tid + q * kThreads;
+        coff[q] = -2;                       /* not owned */
+        if (j < twz) {
+            coff[q] = -1;                   /* zero padding */
+            if (j < tw) {
+                const int px = j / C, c = j - px * C;
+                coff[q] = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
+            }
+        }
+    }
+
+    for (int rb = 0; rb < th; rb += kTB) {
+        const int nrows = th - rb < kTB ? th - rb : kTB;
+        for (int row = 0; row < nrows; row++) {
+            const int yy = fast_clamp(y0 - r + rb + row, 0, H - 1);
+            const T *grow = src + (size_t)yy * W * C;
+            float *trow = tile + row * twp + tid;
+#pragma unroll
+            for (int q = 0; q < kNQ; q++) {
+                if (coff[q] >= 0)
+                    trow[q * kThreads] = fast_px<T>::load(grow + coff[q]);
+                else if (coff[q] == -1)
+                    trow[q * kThreads] = 0.0f;
+            }
+        }
+        __syncthreads();
+        /* horizontal pass over the staged rows (blockwise.py:151) */
+        for (int task = tid; task < nrows * nseg; task += kThreads) {
+            const int row = task / nseg, seg = task - row * nseg;
+            h_task<C>(tile + row * twp + seg * SEG, wts, nchunk,
+                      interm + (size_t)(rb + row) * IWP + seg * SEG);
+        }
+        __syncthreads();
+    }
+
+    /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) ------------ */
+    const int ncg = (fw * C + 3) >> 2;
+    const int nrg = (fh + kRV - 1) / kRV;
+    for (int task = tid; task < ncg * nrg; task += kThreads) {
+        const int rg = task / ncg, cg = task - rg * ncg;
+        float acc[kRV][4];
+        v_task(interm + (size_t)(rg * kRV) * IWP + cg * 4, IWP, wts, nchunk, acc);
+#pragma unroll
+        for (int j = 0; j < kRV; j++) {
+            const int y = rg * kRV + j;
+            if (y < fh) {
+                T *orow = dst + ((size_t)(y0 + y) * W + x0) * C + cg * 4;
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    if (cg * 4 + i < fw * C) orow[i] = fast_px<T>::store(acc[j][i]);
+            }
+        }
+    }
+}
+
+struct fast_layout {
+    int wts_floats, twp, irows;
+    size_t smem;
+};
+
+template <int C> fast_layout fast_layout_for(int bound_length)
+{
+    constexpr int SEG = 8 * C;
+    constexpr int NSEG = (kSub * C + SEG - 1) / SEG;
+    constexpr int IWP = NSEG * SEG + 4;
+    fast_layout l;
+    const int nchunk = (bound_length + 3) / 4;
+    l.wts_floats = 4 * nchunk;
+    int twp = C * (8 * NSEG + 4 + 4 * nchunk);
+    twp = (twp + 3) & ~3;
+    if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
+    l.twp = twp;
+    l.irows = kSub + 4 + 4 * nchunk;
+    l.smem = ((size_t)l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
+    return l;
+}
+
+template <typename T, int C>
+cudaError_t launch_fast(const fk_plan_dev &pd, const void *in, void *out, int n_frames,
+                        int bound_length, size_t max_smem, cudaStream_t s, bool *taken)
+{
+    const fast_layout l = fast_layout_for<C>(bound_length);
+    *taken = false;
+    if (l.smem > max_smem || l.twp > kNQ * kThreads) return cudaSuccess;
+    const int nsub = (pd.fragment + kSub - 1) / kSub;
+    const long long blocks = (long long)n_frames * pd.cap * nsub * nsub;
+    if (blocks > 0x7fffffffLL) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fk_blur_fast<T, C>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l.smem);
+    if (e != cudaSuccess) return e;
+    fk_blur_fast<T, C><<<(unsigned)blocks, kThreads, l.smem, s>>>(
+        pd, (const T *)in, (T *)out, n_frames, nsub, l.wts_floats, l.twp, l.irows);
+    *taken = true;
+    return cudaGetLastError();
+}
+
+} // namespace
+
+/* Returns cudaSuccess with *taken = false when the fast kernel cannot take the launch. */
+cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
+                                int n_frames, int channels, int is_f32, int bound_length,
+                                cudaStream_t s, bool *taken)
+{
+    const size_t max_smem = h->prop.sharedMemPerBlockOptin;
+    if (channels == 3)
+        return is_f32 ? launch_fast<float, 3>(pd, in, out, n_frames, bound_length, max_smem, s, taken)
+                      : launch_fast<uint8_t, 3>(pd, in, out, n_frames, bound_length, max_smem, s, taken);
+    return is_f32 ? launch_fast<float, 1>(pd, in, out, n_frames, bound_length, max_smem, s, taken)
+                  : launch_fast<uint8_t, 1>(pd, in, out, n_frames, bound_length, max_smem, s, taken);
+}

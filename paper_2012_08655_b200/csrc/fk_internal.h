@@ -90,6 +90,9 @@ cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s);
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,
                            cudaStream_t s, int *launches);
+cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
+                                int n_frames, int channels, int is_f32, int bound_length,
+                                cudaStream_t s, bool *taken);
 cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s);
 
 /* Host replica of the grid geometry (tiling.py:15-28). */

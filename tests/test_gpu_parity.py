@@ -403,3 +403,27 @@ def test_long_filters_grow_the_lut_and_strip_path():
     assert stats.max_filter > 255
     ref, _ = fo.c_foveate(img, fo.OracleParams(**kw), threads=8)
     assert maxdiff(out.data, ref) <= U8_TOL
+
+
+def test_fast_and_generic_kernels_agree_bit_for_bit():
+    """Both kernels accumulate taps in the same order, so they must agree exactly."""
+    eng = fk.get_engine(0)
+    rng = np.random.default_rng(77)
+    cases = [((270, 480, 3), 32, torch.uint8), ((200, 333, 1), 16, torch.uint8),
+             ((150, 260, 3), 64, torch.float32), ((97, 131, 3), 8, torch.float32),
+             ((128, 128, 1), 100, torch.float32)]
+    for shape, F, dtype in cases:
+        n = 3
+        if dtype == torch.uint8:
+            frames = torch.from_numpy(rng.integers(0, 256, (n, *shape), dtype=np.uint8)).cuda()
+        else:
+            frames = torch.from_numpy(rng.random((n, *shape), dtype=np.float32)).cuda()
+        fix = np.stack([rng.uniform(0, shape[1], n), rng.uniform(0, shape[0], n)], axis=1)
+        p = fk.FoveationParams(fragment_size=F, strength=1.3)
+        try:
+            eng.set_kernel_variant(1)
+            a = fk.foveate_batch(frames, fix, p).clone()
+        finally:
+            eng.set_kernel_variant(0)
+        b = fk.foveate_batch(frames, fix, p)
+        assert torch.equal(a, b), (shape, F, dtype)
