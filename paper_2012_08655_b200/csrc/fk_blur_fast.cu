@@ -7,9 +7,14 @@
  *
  *   work item   one <=32x32 sub-rectangle of a fragment (all of it for F <= 32), one CTA
  *               of 128 threads per item, items ordered by descending tap count per frame.
- *   staging     the tile is converted to fp32 once and staged in shared memory in blocks
- *               of 32 tile rows; row pitch = 4 (mod 8) floats so LDS.128 from 8 different
- *               rows hits 8 different bank groups.
+ *   staging     uint8 frames: the tile (fragment + halo) is fetched 32 rows at a time by
+ *               TMA (cp.async.bulk.tensor, 128-byte x 32-row boxes, zero fill outside the
+ *               image) into a raw byte buffer while the previous 32 rows are being
+ *               filtered; a short pass converts bytes to fp32 (PRMT + FADD) into the
+ *               working tile and applies clamp-to-edge by index.  float32 frames and
+ *               buffers TMA cannot describe are staged with plain loads.
+ *               Tile row pitch = 4 (mod 8) floats so LDS.128 from 8 different rows hits
+ *               8 different bank groups.
  *   H pass      one task = 8 pixels x C channels of one tile row (8C accumulators).  The
  *               taps are walked in chunks of 4; the input window lives in 12C registers
  *               used as a ring with compile-time indices, refilled with LDS.128 as soon
@@ -19,17 +24,21 @@
  *               of the intermediate (128 FFMA per 5 LDS.128).
  *
  * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can
- * touch is zero-filled so 0 * garbage never produces a NaN.
+ * touch holds a finite value so 0 * garbage never produces a NaN.
  */
+#include <cuda.h>
+
 #include "fk_internal.h"
 
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kTB = 32;   /* tile rows staged per block */
-constexpr int kRV = 8;    /* output rows per V task */
-constexpr int kSub = 32;  /* sub-rectangle edge */
-constexpr int kNQ = 6;    /* tile columns a thread may own while staging (kNQ * 128 floats) */
+constexpr int kTB = 32;        /* tile rows staged per block */
+constexpr int kRV = 8;         /* output rows per V task */
+constexpr int kSub = 32;       /* sub-rectangle edge */
+constexpr int kNQ = 6;         /* LDG staging: tile columns per thread (kNQ * 128 floats) */
+constexpr int kPanelB = 128;   /* TMA box: bytes per row */
+constexpr int kPanelBytes = kPanelB * kTB;
 
 template <typename T> struct fast_px;
 template <> struct fast_px<uint8_t> {
@@ -61,6 +70,57 @@ __device__ __forceinline__ void fast_span(int extent, int F, int off, int g, int
 __device__ __forceinline__ int fast_clamp(int v, int lo, int hi)
 {
     return v < lo ? lo : (v > hi ? hi : v);
+}
+
+/* ---- TMA / mbarrier plumbing (PTX; SASS: UTMALDG, SYNCS) ------------------------- */
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_LOOP:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra WAIT_DONE;\n\t"
+        "bra WAIT_LOOP;\n\t"
+        "WAIT_DONE:\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1, int c2)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+/* Four bytes of a word to four floats, exactly: PRMT into the mantissa of 2^23, FADD. */
+__device__ __forceinline__ float4 bytes_to_float4(uint32_t w)
+{
+    float4 f;
+    f.x = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440)) - 8388608.0f;
+    f.y = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7441)) - 8388608.0f;
+    f.z = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7442)) - 8388608.0f;
+    f.w = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7443)) - 8388608.0f;
+    return f;
 }
 
 /*
@@ -166,16 +226,26 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
     }
 }
 
-template <typename T, int C>
-__global__ void __launch_bounds__(kThreads, 4)
-fk_blur_fast(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int n_frames,
-             int nsub, int wts_floats, int twp, int irows)
+/*
+ * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
+ *              (W*C, H, N) with 128 x 32 x 1 boxes.
+ * TMA = false: plain-load staging (float32 frames, or buffers TMA cannot describe).
+ */
+template <typename T, int C, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2)
+fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
+             const T *__restrict__ in, T *__restrict__ out, int n_frames, int nsub,
+             int wts_floats, int twp, int npanel_max)
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
     constexpr int IWP = NSEG_MAX * SEG + 4;               /* pitch/4 odd: 100 or 36 */
-    extern __shared__ __align__(16) float smem[];
-    float *wts = smem;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    /* layout: [raw panels][mbarrier][colmap][taps][tile][intermediate] */
+    unsigned char *raw = smem_raw;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
+    int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 16);
+    float *wts = reinterpret_cast<float *>(colmap + (TMA ? twp : 0));
     float *tile = wts + wts_floats;
     float *interm = tile + kTB * twp;
 
@@ -224,6 +294,24 @@ fk_blur_fast(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int 
     const int tw = (fw + 2 * r) * C;                    /* valid tile floats per row */
     const int twz = C * (8 * nseg + 4 + 4 * nchunk);    /* floats the H tasks may touch */
 
+    /* TMA geometry: the box origin is clamped into the image so that every clamped
+     * source row / column of this block lies inside the box. */
+    const bool xin = (x0 - r >= 0) && (x1 + r <= W);
+    const int xs_c = fast_clamp(x0 - r, 0, W - 1);
+    const int npanel = (twz + kPanelB - 1) / kPanelB;
+    auto issue = [&](int rb) {
+        const int ys_c = fast_clamp(y0 - r + rb, 0, H - 1);
+        mbar_expect_tx(bar, (uint32_t)(npanel * kPanelBytes));
+        for (int p = 0; p < npanel; p++)
+            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, xs_c * C + p * kPanelB, ys_c, f);
+    };
+    if (TMA) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            issue(0);
+        }
+    }
+
     {   /* taps, zero-padded; zero rows of the intermediate that padded taps may touch */
         const float *taps = pd.taps + pd.offset[(size_t)f * pd.cap + cell];
         for (int i = tid; i < 4 * nchunk; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
@@ -233,36 +321,86 @@ fk_blur_fast(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int 
         for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
-    /* ---- staging ownership: each thread owns up to kNQ tile columns ------------ */
     int coff[kNQ];
+    if (TMA) {
+        if (!xin) { /* clamp-to-edge by index: tile column -> byte offset inside the box */
+            for (int j = tid; j < twz; j += kThreads) {
+                int m = -1;
+                if (j < tw) {
+                    const int px = j / C, c = j - px * C;
+                    m = (fast_clamp(x0 - r + px, 0, W - 1) - xs_c) * C + c;
+                }
+                colmap[j] = m;
+            }
+        }
+        __syncthreads(); /* mbarrier init + colmap visible to all threads */
+    } else {
+        /* plain-load staging: each thread owns up to kNQ tile columns */
 #pragma unroll
-    for (int q = 0; q < kNQ; q++) {
-        const int j = tid + q * kThreads;
-        coff[q] = -2;                       /* not owned */
-        if (j < twz) {
-            coff[q] = -1;                   /* zero padding */
-            if (j < tw) {
-                const int px = j / C, c = j - px * C;
-                coff[q] = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
+        for (int q = 0; q < kNQ; q++) {
+            const int j = tid + q * kThreads;
+            coff[q] = -2; /* not owned */
+            if (j < twz) {
+                coff[q] = -1; /* zero padding */
+                if (j < tw) {
+                    const int px = j / C, c = j - px * C;
+                    coff[q] = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
+                }
             }
         }
     }
 
+    uint32_t phase = 0;
+    const int warp = tid >> 5, lane = tid & 31;
     for (int rb = 0; rb < th; rb += kTB) {
         const int nrows = th - rb < kTB ? th - rb : kTB;
-        for (int row = 0; row < nrows; row++) {
-            const int yy = fast_clamp(y0 - r + rb + row, 0, H - 1);
-            const T *grow = src + (size_t)yy * W * C;
-            float *trow = tile + row * twp + tid;
+        if (TMA) {
+            const int ys = y0 - r + rb;
+            const int ys_c = fast_clamp(ys, 0, H - 1);
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            if (xin) {
+                const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
+                for (int row = warp; row < nrows; row += kThreads / 32) {
+                    const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
+                    const uint32_t *rp = raw32 + rr * (kPanelB / 4) + lane;
+                    float4 *tp = reinterpret_cast<float4 *>(tile + row * twp) + lane;
+                    for (int p = 0; p < npanel; p++) {
+                        if (4 * (lane + 32 * p) < twz)
+                            tp[32 * p] = bytes_to_float4(rp[p * (kPanelBytes / 4)]);
+                    }
+                }
+            } else {
+                for (int row = warp; row < nrows; row += kThreads / 32) {
+                    const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
+                    const unsigned char *rp = raw + rr * kPanelB;
+                    float *tp = tile + row * twp;
+                    for (int j = lane; j < twz; j += 32) {
+                        const int m = colmap[j];
+                        tp[j] = m >= 0
+                                    ? (float)rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))]
+                                    : 0.0f;
+                    }
+                }
+            }
+        } else {
+            for (int row = 0; row < nrows; row++) {
+                const int yy = fast_clamp(y0 - r + rb + row, 0, H - 1);
+                const T *grow = src + (size_t)yy * W * C;
+                float *trow = tile + row * twp + tid;
 #pragma unroll
-            for (int q = 0; q < kNQ; q++) {
-                if (coff[q] >= 0)
-                    trow[q * kThreads] = fast_px<T>::load(grow + coff[q]);
-                else if (coff[q] == -1)
-                    trow[q * kThreads] = 0.0f;
+                for (int q = 0; q < kNQ; q++) {
+                    if (coff[q] >= 0)
+                        trow[q * kThreads] = fast_px<T>::load(grow + coff[q]);
+                    else if (coff[q] == -1)
+                        trow[q * kThreads] = 0.0f;
+                }
             }
         }
         __syncthreads();
+        if (TMA) { /* the raw buffer is free again: fetch the next 32 rows during the H pass */
+            if (tid == 0 && rb + kTB < th) issue(rb + kTB);
+        }
         /* horizontal pass over the staged rows (blockwise.py:151) */
         for (int task = tid; task < nrows * nseg; task += kThreads) {
             const int row = task / nseg, seg = task - row * nseg;
@@ -293,11 +431,11 @@ fk_blur_fast(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int 
 }
 
 struct fast_layout {
-    int wts_floats, twp, irows;
+    int wts_floats, twp, irows, npanel;
     size_t smem;
 };
 
-template <int C> fast_layout fast_layout_for(int bound_length)
+template <int C> fast_layout fast_layout_for(int bound_length, bool tma)
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG = (kSub * C + SEG - 1) / SEG;
@@ -305,45 +443,98 @@ template <int C> fast_layout fast_layout_for(int bound_length)
     fast_layout l;
     const int nchunk = (bound_length + 3) / 4;
     l.wts_floats = 4 * nchunk;
-    int twp = C * (8 * NSEG + 4 + 4 * nchunk);
-    twp = (twp + 3) & ~3;
+    const int twz = C * (8 * NSEG + 4 + 4 * nchunk);
+    int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
     l.irows = kSub + 4 + 4 * nchunk;
-    l.smem = ((size_t)l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
+    l.npanel = tma ? (twz + kPanelB - 1) / kPanelB : 0;
+    l.smem = (size_t)l.npanel * kPanelBytes + 16 + (tma ? (size_t)twp * sizeof(int) : 0) +
+             ((size_t)l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
     return l;
 }
 
-template <typename T, int C>
-cudaError_t launch_fast(const fk_plan_dev &pd, const void *in, void *out, int n_frames,
-                        int bound_length, size_t max_smem, cudaStream_t s, bool *taken)
+typedef CUresult (*encode_tiled_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_tiled_fn get_encode_tiled()
 {
-    const fast_layout l = fast_layout_for<C>(bound_length);
+    static encode_tiled_fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (encode_tiled_fn)p;
+    }
+    return fn;
+}
+
+/* 3-D byte tensor (W*C, H, N) over the input batch; false if TMA cannot describe it. */
+bool make_tensor_map(CUtensorMap *map, const void *in, int W, int H, int C, int n_frames)
+{
+    encode_tiled_fn enc = get_encode_tiled();
+    const size_t pitch = (size_t)W * C;
+    if (!enc || ((uintptr_t)in & 15) != 0 || (pitch & 15) != 0) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)H, (cuuint64_t)n_frames};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * H};
+    cuuint32_t box[3] = {(cuuint32_t)kPanelB, (cuuint32_t)kTB, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(in), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <typename T, int C, bool TMA>
+cudaError_t launch_fast(const CUtensorMap &map, const fk_plan_dev &pd, const void *in, void *out,
+                        int n_frames, int bound_length, size_t max_smem, cudaStream_t s,
+                        bool *taken)
+{
+    const fast_layout l = fast_layout_for<C>(bound_length, TMA);
     *taken = false;
-    if (l.smem > max_smem || l.twp > kNQ * kThreads) return cudaSuccess;
+    if (l.smem > max_smem || (!TMA && l.twp > kNQ * kThreads)) return cudaSuccess;
     const int nsub = (pd.fragment + kSub - 1) / kSub;
     const long long blocks = (long long)n_frames * pd.cap * nsub * nsub;
     if (blocks > 0x7fffffffLL) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(fk_blur_fast<T, C>,
+    cudaError_t e = cudaFuncSetAttribute(fk_blur_fast<T, C, TMA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l.smem);
     if (e != cudaSuccess) return e;
-    fk_blur_fast<T, C><<<(unsigned)blocks, kThreads, l.smem, s>>>(
-        pd, (const T *)in, (T *)out, n_frames, nsub, l.wts_floats, l.twp, l.irows);
+    fk_blur_fast<T, C, TMA><<<(unsigned)blocks, kThreads, l.smem, s>>>(
+        map, pd, (const T *)in, (T *)out, n_frames, nsub, l.wts_floats, l.twp, l.npanel);
     *taken = true;
     return cudaGetLastError();
 }
 
 } // namespace
 
-/* Returns cudaSuccess with *taken = false when the fast kernel cannot take the launch. */
+/* Returns cudaSuccess with *taken = false when the fast kernel cannot take the launch.
+ * h->variant: 0 auto, 2 = fast kernel with plain-load staging (no TMA). */
 cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                                 int n_frames, int channels, int is_f32, int bound_length,
                                 cudaStream_t s, bool *taken)
 {
     const size_t max_smem = h->prop.sharedMemPerBlockOptin;
-    if (channels == 3)
-        return is_f32 ? launch_fast<float, 3>(pd, in, out, n_frames, bound_length, max_smem, s, taken)
-                      : launch_fast<uint8_t, 3>(pd, in, out, n_frames, bound_length, max_smem, s, taken);
-    return is_f32 ? launch_fast<float, 1>(pd, in, out, n_frames, bound_length, max_smem, s, taken)
-                  : launch_fast<uint8_t, 1>(pd, in, out, n_frames, bound_length, max_smem, s, taken);
+    CUtensorMap map;
+    memset(&map, 0, sizeof map);
+    if (is_f32) {
+        if (channels == 3)
+            return launch_fast<float, 3, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+        return launch_fast<float, 1, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+    }
+    const bool tma = h->variant != 2 &&
+                     make_tensor_map(&map, in, pd.width, pd.height, channels, n_frames);
+    if (channels == 3) {
+        if (tma)
+            return launch_fast<uint8_t, 3, true>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+        return launch_fast<uint8_t, 3, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+    }
+    if (tma)
+        return launch_fast<uint8_t, 1, true>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+    return launch_fast<uint8_t, 1, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
 }

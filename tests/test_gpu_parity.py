@@ -420,10 +420,39 @@ def test_fast_and_generic_kernels_agree_bit_for_bit():
             frames = torch.from_numpy(rng.random((n, *shape), dtype=np.float32)).cuda()
         fix = np.stack([rng.uniform(0, shape[1], n), rng.uniform(0, shape[0], n)], axis=1)
         p = fk.FoveationParams(fragment_size=F, strength=1.3)
+        outs = {}
         try:
-            eng.set_kernel_variant(1)
-            a = fk.foveate_batch(frames, fix, p).clone()
+            for variant in (1, 2):      # 1 = generic kernel, 2 = fast kernel without TMA
+                eng.set_kernel_variant(variant)
+                outs[variant] = fk.foveate_batch(frames, fix, p).clone()
         finally:
             eng.set_kernel_variant(0)
-        b = fk.foveate_batch(frames, fix, p)
-        assert torch.equal(a, b), (shape, F, dtype)
+        b = fk.foveate_batch(frames, fix, p)   # auto: TMA staging where the buffer allows
+        assert torch.equal(outs[1], b), (shape, F, dtype)
+        assert torch.equal(outs[2], b), (shape, F, dtype)
+
+
+def test_tma_path_border_and_interior_tiles_vs_generic():
+    """uint8 frames whose row pitch is a multiple of 16 bytes take the TMA staging path;
+    corner fixations make most tiles cross the image border (clamp-to-edge by index)."""
+    eng = fk.get_engine(0)
+    rng = np.random.default_rng(5)
+    for (h, w, c), F in (((256, 256, 3), 32), ((96, 160, 3), 16), ((64, 64, 1), 32),
+                         ((540, 960, 3), 32), ((33, 48, 1), 8)):
+        assert (w * c) % 16 == 0
+        n = 4
+        frames = torch.from_numpy(rng.integers(0, 256, (n, h, w, c), dtype=np.uint8)).cuda()
+        fix = np.asarray([[0, 0], [w - 1, h - 1], [w / 2, h / 2], [w - 1, 0]], dtype=np.float64)
+        p = fk.FoveationParams(fragment_size=F, strength=1.5)
+        try:
+            eng.set_kernel_variant(1)
+            ref = fk.foveate_batch(frames, fix, p).clone()
+        finally:
+            eng.set_kernel_variant(0)
+        got = fk.foveate_batch(frames, fix, p)
+        assert torch.equal(ref, got), ((h, w, c), F)
+        # a view at a 16-byte-misaligned offset falls back to plain-load staging
+        flat = torch.empty(frames.numel() + 16, dtype=torch.uint8, device="cuda")
+        view = flat[4:4 + frames.numel()].view_as(frames)
+        view.copy_(frames)
+        assert torch.equal(fk.foveate_batch(view, fix, p), ref)
