@@ -298,12 +298,16 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
      * source row / column of this block lies inside the box. */
     const bool xin = (x0 - r >= 0) && (x1 + r <= W);
     const int xs_c = fast_clamp(x0 - r, 0, W - 1);
-    const int npanel = (twz + kPanelB - 1) / kPanelB;
+    /* TMA needs the box to start on a 16-byte boundary of the row: fetch from the
+     * aligned-down byte and skip `skew` bytes when converting. */
+    const int c0a = (xs_c * C) & ~15;
+    const int skew = xs_c * C - c0a;
+    const int npanel = (skew + twz + 4 + kPanelB - 1) / kPanelB;
     auto issue = [&](int rb) {
         const int ys_c = fast_clamp(y0 - r + rb, 0, H - 1);
         mbar_expect_tx(bar, (uint32_t)(npanel * kPanelBytes));
         for (int p = 0; p < npanel; p++)
-            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, xs_c * C + p * kPanelB, ys_c, f);
+            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, f);
     };
     if (TMA) {
         if (tid == 0) {
@@ -328,7 +332,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 int m = -1;
                 if (j < tw) {
                     const int px = j / C, c = j - px * C;
-                    m = (fast_clamp(x0 - r + px, 0, W - 1) - xs_c) * C + c;
+                    m = skew + (fast_clamp(x0 - r + px, 0, W - 1) - xs_c) * C + c;
                 }
                 colmap[j] = m;
             }
@@ -360,14 +364,18 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             mbar_wait(bar, phase);
             phase ^= 1;
             if (xin) {
+                /* tile word wj = raw bytes [skew + 4 wj, +4): two aligned words, funnel shift */
                 const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
+                const int wsk = skew >> 2, bsh = (skew & 3) * 8;
                 for (int row = warp; row < nrows; row += kThreads / 32) {
                     const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
-                    const uint32_t *rp = raw32 + rr * (kPanelB / 4) + lane;
-                    float4 *tp = reinterpret_cast<float4 *>(tile + row * twp) + lane;
-                    for (int p = 0; p < npanel; p++) {
-                        if (4 * (lane + 32 * p) < twz)
-                            tp[32 * p] = bytes_to_float4(rp[p * (kPanelBytes / 4)]);
+                    const uint32_t *rp = raw32 + rr * (kPanelB / 4);
+                    float4 *tp = reinterpret_cast<float4 *>(tile + row * twp);
+                    for (int wj = lane; 4 * wj < twz; wj += 32) {
+                        const int w0 = wj + wsk, w1 = w0 + 1;
+                        const uint32_t lo = rp[(w0 >> 5) * (kPanelBytes / 4) + (w0 & 31)];
+                        const uint32_t hi = rp[(w1 >> 5) * (kPanelBytes / 4) + (w1 & 31)];
+                        tp[wj] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
                     }
                 }
             } else {
@@ -448,7 +456,7 @@ template <int C> fast_layout fast_layout_for(int bound_length, bool tma)
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
     l.irows = kSub + 4 + 4 * nchunk;
-    l.npanel = tma ? (twz + kPanelB - 1) / kPanelB : 0;
+    l.npanel = tma ? (15 + twz + 4 + kPanelB - 1) / kPanelB : 0;
     l.smem = (size_t)l.npanel * kPanelBytes + 16 + (tma ? (size_t)twp * sizeof(int) : 0) +
              ((size_t)l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
     return l;
