@@ -241,7 +241,11 @@ def run_gpu(args):
     frames = torch.randint(0, 256, (n, H, W, C), dtype=torch.uint8, device="cuda", generator=gen)
     out = torch.empty_like(frames)
     fixes = moving_fixations(n)
-    fix_dev = torch.from_numpy(fixes).cuda()
+    if args.fixation == "centre":       # exploration only; the reported workload is "moving"
+        fixes[:] = (W / 2.0, H / 2.0)
+    elif args.fixation == "corner":
+        fixes[:] = (0.0, 0.0)
+    fix_dev = fixes if args.fix_host else torch.from_numpy(fixes).cuda()
     plan = eng.plan_for((W, H), F, n)
     stream = torch.cuda.current_stream()
 
@@ -370,6 +374,10 @@ def main():
     ap.add_argument("--e2e-frames", type=int, default=BATCH)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fixation", default="moving", choices=["moving", "centre", "corner"],
+                    help="exploration only; BASELINE configs[1] is 'moving'")
+    ap.add_argument("--fix-host", action="store_true",
+                    help="exploration only: pass fixations from host memory each step")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

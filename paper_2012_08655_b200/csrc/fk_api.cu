@@ -232,6 +232,8 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     if (fragment_size < 4)
         return fk_fail(h, FK_EINVAL, "fragment_size must be >= 4, got %d", fragment_size);
     if (max_frames < 1) return fk_fail(h, FK_EINVAL, "max_frames must be >= 1");
+    if (width > 65535 || height > 65535)
+        return fk_fail(h, FK_EINVAL, "images larger than 65535 pixels per side are not supported");
     FK_CUDA(h, cudaSetDevice(h->device));
     fk_plan *p = new (std::nothrow) fk_plan();
     if (!p) return fk_fail(h, FK_ENOMEM, "out of host memory");
@@ -244,6 +246,12 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     d.height = height;
     d.fragment = fragment_size;
     d.cap = gwm * ghm;
+    d.nsub = (fragment_size + FK_RECT - 1) / FK_RECT;
+    d.items_cap = (size_t)max_frames * d.cap * d.nsub * d.nsub;
+    if ((double)d.items_cap > 2.0e9) {
+        delete p;
+        return fk_fail(h, FK_EINVAL, "batch too large: %d frames x %d fragments", max_frames, d.cap);
+    }
     const size_t cells = (size_t)max_frames * d.cap;
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = cudaMalloc(&d.sigma, cells * sizeof(double));
@@ -251,6 +259,8 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     if (e == cudaSuccess) e = cudaMalloc(&d.length, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.offset, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.order, cells * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.items, FK_NCLASS * d.items_cap * sizeof(fk_item));
+    if (e == cudaSuccess) e = cudaMalloc(&d.counters, 2 * FK_NCLASS * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.meta, (size_t)max_frames * FK_META_WORDS * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&p->fix_dev, (size_t)max_frames * 2 * sizeof(double));
     if (e != cudaSuccess) {
@@ -271,6 +281,8 @@ int fk_plan_destroy(fk_plan *p)
     cudaFree(p->d.length);
     cudaFree(p->d.offset);
     cudaFree(p->d.order);
+    cudaFree(p->d.items);
+    cudaFree(p->d.counters);
     cudaFree(p->d.meta);
     cudaFree(p->fix_dev);
     cudaFree(p->custom_taps);
@@ -333,6 +345,7 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     }
     p->d.taps = h->lut32;
     p->custom = 0;
+    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, s));
     h->launches++;
     p->n_frames = n_frames;
@@ -391,6 +404,7 @@ int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_
     FK_CUDA(h, cudaStreamSynchronize(s));
     p->d.taps = p->custom_taps;
     p->custom = 1;
+    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
     FK_CUDA(h, fk_launch_order_custom(p->d, s));
     h->launches++;
     p->n_frames = 1;

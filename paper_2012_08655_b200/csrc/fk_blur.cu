@@ -1,5 +1,6 @@
 /*
- * fk_blur.cu -- per-fragment separable Gaussian blur (sm_100a).
+ * fk_blur.cu -- per-fragment separable Gaussian blur (sm_100a): dispatcher, the generic
+ * kernel and the FP32 probe.
  *
  * Replaces blockwise.py:136-186 (_render_cell / render) and convolve.py:9-15
  * (quantize_u8): clamp-to-edge gather of the fragment plus its halo, horizontal pass
@@ -10,7 +11,8 @@
  * Kernels
  *   fk_blur_generic  any tap count, any geometry: intermediate in shared memory,
  *                    input read straight from global/L2.  Correctness baseline and
- *                    fallback for fragments the fast kernel does not take.
+ *                    fallback for the work classes the fast kernel (fk_blur_fast.cu)
+ *                    does not take.
  */
 #include "fk_internal.h"
 
@@ -32,103 +34,95 @@ template <> struct fk_px<float> {
     static __device__ __forceinline__ float store(float v) { return v; }
 };
 
-__device__ __forceinline__ void fk_span_dev(int extent, int F, int off, int g, int &a, int &b)
-{
-    const int lead = off > 0 ? 1 : 0;
-    if (lead && g == 0) {
-        a = 0;
-        b = off < extent ? off : extent;
-    } else {
-        a = off + (g - lead) * F;
-        b = a + F < extent ? a + F : extent;
-    }
-}
-
 __device__ __forceinline__ int fk_clamp(int v, int lo, int hi)
 {
     return v < lo ? lo : (v > hi ? hi : v);
 }
 
 /*
- * One CTA per (frame, order slot).  Shared memory: taps[w_floats] then the H-pass
- * intermediate, interm_floats floats; fragments whose (fh + 2r) * fw * C intermediate
- * does not fit are processed in column strips.
+ * Persistent CTAs walk one class list through its atomic cursor.  Shared memory:
+ * taps[w_floats] then the H-pass intermediate, interm_floats floats; rectangles whose
+ * (fh + 2r) * fw * C intermediate does not fit are processed in column strips.
  */
 template <typename T>
 __global__ void __launch_bounds__(256)
-fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int n_frames,
-                int C, int w_floats, int interm_floats)
+fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int klass, int C,
+                int w_floats, int interm_floats)
 {
     extern __shared__ float smem[];
+    __shared__ int s_idx;
     float *wts = smem;
     float *interm = smem + w_floats;
-
-    const int f = blockIdx.x / pd.cap;
-    const int slot = blockIdx.x - f * pd.cap;
-    if (f >= n_frames) return;
-    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
-    if (meta[FK_META_STATUS] != 0) return;
-    const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
-    if (slot >= gw * gh) return;
-    const int cell = (int)pd.order[(size_t)f * pd.cap + slot];
-    const int gy = cell / gw, gx = cell - gy * gw;
+    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
+    const int n_items = pd.counters[klass];
+    int *cursor = pd.counters + FK_NCLASS + klass;
     const int W = pd.width, H = pd.height;
-    int x0, x1, y0, y1;
-    fk_span_dev(W, pd.fragment, meta[FK_META_SX], gx, x0, x1);
-    fk_span_dev(H, pd.fragment, meta[FK_META_SY], gy, y0, y1);
-    const int L = pd.length[(size_t)f * pd.cap + cell];
-    const int fw = x1 - x0, fh = y1 - y0;
-    const size_t frame_off = (size_t)f * H * W * C;
-    const T *src = in + frame_off;
-    T *dst = out + frame_off;
     const int tid = threadIdx.x, nt = blockDim.x;
 
-    if (L == 1) { /* blockwise.py:141-143: identity fragments are copied through */
-        const int rowlen = fw * C;
-        for (int i = tid; i < fh * rowlen; i += nt) {
-            const int y = i / rowlen, c = i - y * rowlen;
-            const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
-            dst[o] = src[o];
-        }
-        return;
-    }
-    const int r = (L - 1) >> 1;
-    const float *taps = pd.taps + pd.offset[(size_t)f * pd.cap + cell];
-    for (int i = tid; i < L; i += nt) wts[i] = taps[i];
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_idx = atomicAdd(cursor, 1);
+        __syncthreads();
+        const int idx = s_idx;
+        if (idx >= n_items) break;
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
+        const int fw = (int)(q.z & 0xffu), fh = (int)(q.z >> 21);
+        if (fw == 0 || fh == 0) continue;
+        const int f = (int)q.x;
+        const int x0 = (int)(q.y & 0xffffu), y0 = (int)(q.y >> 16);
+        const int x1 = x0 + fw;
+        const int L = (int)((q.z >> 8) & 0x1fffu);
+        const size_t frame_off = (size_t)f * H * W * C;
+        const T *src = in + frame_off;
+        T *dst = out + frame_off;
 
-    const int th = fh + 2 * r;
-    int ws = interm_floats / (th * C);
-    ws = ws > fw ? fw : ws;
-    if (ws < 1) return; /* host sizes the buffer so that this cannot happen */
-    __syncthreads();
-
-    for (int xs = x0; xs < x1; xs += ws) {
-        const int sw = (x1 - xs) < ws ? (x1 - xs) : ws;
-        const int cols = sw * C;
-        /* horizontal pass over every tile row (blockwise.py:151) */
-        for (int i = tid; i < th * cols; i += nt) {
-            const int ty = i / cols, col = i - ty * cols;
-            const int px = col / C, c = col - px * C;
-            const int yy = fk_clamp(y0 - r + ty, 0, H - 1);
-            const T *row = src + (size_t)yy * W * C + c;
-            const int xb = xs + px - r;
-            float acc = 0.0f;
-            for (int k = 0; k < L; k++) {
-                const int xx = fk_clamp(xb + k, 0, W - 1);
-                acc = fmaf(wts[k], fk_px<T>::load(row + (size_t)xx * C), acc);
+        if (L == 1) { /* blockwise.py:141-143: identity fragments are copied through */
+            const int rowlen = fw * C;
+            for (int i = tid; i < fh * rowlen; i += nt) {
+                const int y = i / rowlen, c = i - y * rowlen;
+                const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
+                dst[o] = src[o];
             }
-            interm[i] = acc;
+            continue;
         }
+        const int r = (L - 1) >> 1;
+        const float *taps = pd.taps + q.w;
+        for (int i = tid; i < L; i += nt) wts[i] = taps[i];
+
+        const int th = fh + 2 * r;
+        int ws = interm_floats / (th * C);
+        ws = ws > fw ? fw : ws;
+        if (ws < 1) continue; /* host sizes the buffer so that this cannot happen */
         __syncthreads();
-        /* vertical pass over the real-valued intermediate (blockwise.py:152-153) */
-        for (int i = tid; i < fh * cols; i += nt) {
-            const int y = i / cols, col = i - y * cols;
-            const float *colp = interm + (size_t)y * cols + col;
-            float acc = 0.0f;
-            for (int k = 0; k < L; k++) acc = fmaf(wts[k], colp[(size_t)k * cols], acc);
-            dst[((size_t)(y0 + y) * W + xs) * C + col] = fk_px<T>::store(acc);
+
+        for (int xs = x0; xs < x1; xs += ws) {
+            const int sw = (x1 - xs) < ws ? (x1 - xs) : ws;
+            const int cols = sw * C;
+            /* horizontal pass over every tile row (blockwise.py:151) */
+            for (int i = tid; i < th * cols; i += nt) {
+                const int ty = i / cols, col = i - ty * cols;
+                const int px = col / C, c = col - px * C;
+                const int yy = fk_clamp(y0 - r + ty, 0, H - 1);
+                const T *row = src + (size_t)yy * W * C + c;
+                const int xb = xs + px - r;
+                float acc = 0.0f;
+                for (int k = 0; k < L; k++) {
+                    const int xx = fk_clamp(xb + k, 0, W - 1);
+                    acc = fmaf(wts[k], fk_px<T>::load(row + (size_t)xx * C), acc);
+                }
+                interm[i] = acc;
+            }
+            __syncthreads();
+            /* vertical pass over the real-valued intermediate (blockwise.py:152-153) */
+            for (int i = tid; i < fh * cols; i += nt) {
+                const int y = i / cols, col = i - y * cols;
+                const float *colp = interm + (size_t)y * cols + col;
+                float acc = 0.0f;
+                for (int k = 0; k < L; k++) acc = fmaf(wts[k], colp[(size_t)k * cols], acc);
+                dst[((size_t)(y0 + y) * W + xs) * C + col] = fk_px<T>::store(acc);
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -149,6 +143,34 @@ __global__ void __launch_bounds__(256) fk_fp32_probe(float *out, int iters)
     if (s == 12345.678f) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+template <typename T>
+cudaError_t launch_generic(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
+                           void *out, int channels, int class_length, cudaStream_t s)
+{
+    const int r = (class_length - 1) / 2;
+    const int w_floats = (class_length + 3) & ~3;
+    const size_t max_smem = h->prop.sharedMemPerBlockOptin;
+    /* whole rectangle if it fits in ~96 KB (2 CTAs/SM), else strips down to one column */
+    const long long want = (long long)(FK_RECT + 2 * r) * FK_RECT * channels;
+    long long cap_floats = (96 * 1024) / 4 - w_floats;
+    const long long min_floats = (long long)(FK_RECT + 2 * r) * channels;
+    if (cap_floats < min_floats) cap_floats = min_floats;
+    const long long interm = want < cap_floats ? want : cap_floats;
+    const size_t smem = (size_t)(w_floats + interm) * sizeof(float);
+    if (smem > max_smem) return cudaErrorInvalidConfiguration;
+    auto kernel = fk_blur_generic<T>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    kernel<<<h->prop.multiProcessorCount * occ, 256, smem, s>>>(
+        pd, (const T *)in, (T *)out, klass, channels, w_floats, (int)interm);
+    return cudaGetLastError();
+}
+
 } // namespace
 
 cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s)
@@ -157,48 +179,35 @@ cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream
     return cudaGetLastError();
 }
 
+/*
+ * Render every class list of a plan.  Classes whose shortest possible filter exceeds the
+ * plan's bound are empty by construction and are not launched; longest filters first.
+ * h->variant: 0 = fast kernel with generic fallback, 1 = generic kernel only,
+ * 2 = fast kernel without TMA.
+ */
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,
                            cudaStream_t s, int *launches)
 {
-    if (h->variant != 1) { /* fast path unless the generic kernel is forced */
+    /* rewind the render cursors (the counts stay) */
+    cudaError_t e = cudaMemsetAsync(pd.counters + FK_NCLASS, 0, FK_NCLASS * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    for (int k = FK_NCLASS - 1; k >= 0; k--) {
+        const int lmin = k == 0 ? 1 : fk_class_lmax(k - 1) + 2;
+        if (lmin > bound_length) continue;
+        const int class_length = fk_class_lmax(k) < bound_length ? fk_class_lmax(k) : bound_length;
         bool taken = false;
-        cudaError_t fe = fk_launch_blur_fast(h, pd, in, out, n_frames, channels, is_f32,
-                                             bound_length, s, &taken);
-        if (fe != cudaSuccess) return fe;
-        if (taken) {
-            *launches += 1;
-            return cudaSuccess;
+        if (h->variant != 1 && k < FK_NCLASS - 1) {
+            e = fk_launch_blur_fast(h, pd, k, in, out, n_frames, channels, is_f32, class_length,
+                                    s, &taken);
+            if (e != cudaSuccess) return e;
         }
+        if (!taken) {
+            e = is_f32 ? launch_generic<float>(h, pd, k, in, out, channels, class_length, s)
+                       : launch_generic<uint8_t>(h, pd, k, in, out, channels, class_length, s);
+            if (e != cudaSuccess) return e;
+        }
+        *launches += 1;
     }
-    const int F = pd.fragment;
-    const int r = (bound_length - 1) / 2;
-    const int w_floats = (bound_length + 3) & ~3;
-    const int max_smem = (int)h->prop.sharedMemPerBlockOptin;
-    /* whole fragment if it fits in ~96 KB (2 CTAs/SM), else strips down to one column */
-    long long want = (long long)(F + 2 * r) * F * channels;
-    long long cap_floats = (96 * 1024) / 4 - w_floats;
-    long long min_floats = (long long)(F + 2 * r) * channels;
-    if (cap_floats < min_floats) cap_floats = min_floats;
-    long long interm = want < cap_floats ? want : cap_floats;
-    size_t smem = (size_t)(w_floats + interm) * sizeof(float);
-    if (smem > (size_t)max_smem) return cudaErrorInvalidConfiguration;
-    const long long blocks = (long long)n_frames * pd.cap;
-    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    cudaError_t e;
-    if (is_f32) {
-        e = cudaFuncSetAttribute(fk_blur_generic<float>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        fk_blur_generic<float><<<(unsigned)blocks, 256, smem, s>>>(
-            pd, (const float *)in, (float *)out, n_frames, channels, w_floats, (int)interm);
-    } else {
-        e = cudaFuncSetAttribute(fk_blur_generic<uint8_t>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        fk_blur_generic<uint8_t><<<(unsigned)blocks, 256, smem, s>>>(
-            pd, (const uint8_t *)in, (uint8_t *)out, n_frames, channels, w_floats, (int)interm);
-    }
-    *launches += 1;
-    return cudaGetLastError();
+    return cudaSuccess;
 }

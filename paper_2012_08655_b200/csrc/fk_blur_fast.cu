@@ -5,16 +5,19 @@
  * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
  * (convolve.py:15).  What differs from fk_blur_generic is only how the work is laid out:
  *
- *   work item   one <=32x32 sub-rectangle of a fragment (all of it for F <= 32), one CTA
- *               of 128 threads per item, items ordered by descending tap count per frame.
- *   staging     uint8 frames: the tile (fragment + halo) is fetched 32 rows at a time by
- *               TMA (cp.async.bulk.tensor, 128-byte x 32-row boxes, zero fill outside the
- *               image) into a raw byte buffer while the previous 32 rows are being
- *               filtered; a short pass converts bytes to fp32 (PRMT + FADD) into the
- *               working tile and applies clamp-to-edge by index.  float32 frames and
- *               buffers TMA cannot describe are staged with plain loads.
- *               Tile row pitch = 4 (mod 8) floats so LDS.128 from 8 different rows hits
- *               8 different bank groups.
+ *   work items  rectangles of at most 32x32 pixels with one filter each, taken from the
+ *               plan's per-class lists (fk_internal.h) by persistent CTAs of 128 threads
+ *               through an atomic cursor; the launch for a class sizes its shared memory
+ *               for that class's longest filter, so short filters get more CTAs per SM.
+ *   staging     uint8 frames: the tile (rectangle + halo) is fetched 32 rows at a time by
+ *               TMA (cp.async.bulk.tensor, 128-byte x 32-row boxes starting on a 16-byte
+ *               boundary, zero fill outside the image) into a raw byte buffer while the
+ *               previous 32 rows are being filtered, and the first block of the NEXT item
+ *               is fetched during the vertical pass; a short pass converts bytes to fp32
+ *               (funnel shift + PRMT + FADD) into the working tile and applies
+ *               clamp-to-edge by index.  float32 frames and buffers TMA cannot describe
+ *               are staged with plain loads.  Tile row pitch = 4 (mod 8) floats so
+ *               LDS.128 from 8 different rows hits 8 different bank groups.
  *   H pass      one task = 8 pixels x C channels of one tile row (8C accumulators).  The
  *               taps are walked in chunks of 4; the input window lives in 12C registers
  *               used as a ring with compile-time indices, refilled with LDS.128 as soon
@@ -35,37 +38,29 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kTB = 32;        /* tile rows staged per block */
 constexpr int kRV = 8;         /* output rows per V task */
-constexpr int kSub = 32;       /* sub-rectangle edge */
+constexpr int kSub = FK_RECT;   /* rectangle edge */
 constexpr int kNQ = 6;         /* LDG staging: tile columns per thread (kNQ * 128 floats) */
 constexpr int kPanelB = 128;   /* TMA box: bytes per row */
 constexpr int kPanelBytes = kPanelB * kTB;
+constexpr int kPanelWords = kPanelBytes / 4;
+constexpr int kMaxPanels = 5;  /* (15 + twz + 4) / 128 for the longest fast-path filter */
+constexpr int kFetchTid = 96;  /* lane 0 of the last warp: it has no V-pass task */
 
 template <typename T> struct fast_px;
 template <> struct fast_px<uint8_t> {
     static __device__ __forceinline__ float load(const uint8_t *p) { return (float)__ldg(p); }
     static __device__ __forceinline__ uint8_t store(float v)
     {
-        v = floorf(v + 0.5f); /* convolve.py:15 */
-        v = fminf(fmaxf(v, 0.0f), 255.0f);
-        return (uint8_t)v;
+        /* convolve.py:15: clip(floor(v + 0.5), 0, 255); cvt.rmi saturates to [0, 255] */
+        uint32_t u;
+        asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(u) : "f"(v + 0.5f));
+        return (uint8_t)u;
     }
 };
 template <> struct fast_px<float> {
     static __device__ __forceinline__ float load(const float *p) { return __ldg(p); }
     static __device__ __forceinline__ float store(float v) { return v; }
 };
-
-__device__ __forceinline__ void fast_span(int extent, int F, int off, int g, int &a, int &b)
-{
-    const int lead = off > 0 ? 1 : 0;
-    if (lead && g == 0) {
-        a = 0;
-        b = off < extent ? off : extent;
-    } else {
-        a = off + (g - lead) * F;
-        b = a + F < extent ? a + F : extent;
-    }
-}
 
 __device__ __forceinline__ int fast_clamp(int v, int lo, int hi)
 {
@@ -226,6 +221,13 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
     }
 }
 
+/* Decoded work item, kept in shared memory (two slots: current and prefetched). */
+struct item_desc {
+    int valid;
+    int f, x0, y0, fw, fh, L;
+    uint32_t taps_off;
+};
+
 /*
  * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
  *              (W*C, H, N) with 128 x 32 x 1 boxes.
@@ -234,207 +236,246 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
 template <typename T, int C, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
 fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
-             const T *__restrict__ in, T *__restrict__ out, int n_frames, int nsub,
-             int wts_floats, int twp, int npanel_max)
+             const T *__restrict__ in, T *__restrict__ out, int klass, int wts_floats, int twp,
+             int npanel_max)
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
     constexpr int IWP = NSEG_MAX * SEG + 4;               /* pitch/4 odd: 100 or 36 */
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw panels][mbarrier][colmap][taps][tile][intermediate] */
+    /* layout: [raw panels][mbarrier 16 B][2 item slots][colmap][taps][tile][intermediate] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
-    int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 16);
+    item_desc *slots = reinterpret_cast<item_desc *>(reinterpret_cast<unsigned char *>(bar) + 16);
+    int *colmap = reinterpret_cast<int *>(slots + 2);
     float *wts = reinterpret_cast<float *>(colmap + (TMA ? twp : 0));
     float *tile = wts + wts_floats;
     float *interm = tile + kTB * twp;
 
-    /* ---- decode the work item ------------------------------------------------ */
-    const int nsub2 = nsub * nsub;
-    const unsigned item = blockIdx.x / nsub2;
-    const int sub = blockIdx.x - item * nsub2;
-    const int f = item / pd.cap;
-    const int slot = item - f * pd.cap;
-    if (f >= n_frames) return;
-    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
-    if (meta[FK_META_STATUS] != 0) return;
-    const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
-    if (slot >= gw * gh) return;
-    const int cell = (int)pd.order[(size_t)f * pd.cap + slot];
-    const int gy = cell / gw, gx = cell - gy * gw;
     const int W = pd.width, H = pd.height;
-    int cx0, cx1, cy0, cy1;
-    fast_span(W, pd.fragment, meta[FK_META_SX], gx, cx0, cx1);
-    fast_span(H, pd.fragment, meta[FK_META_SY], gy, cy0, cy1);
-    const int sby = sub / nsub, sbx = sub - sby * nsub;
-    const int x0 = cx0 + sbx * kSub, y0 = cy0 + sby * kSub;
-    if (x0 >= cx1 || y0 >= cy1) return;
-    const int x1 = x0 + kSub < cx1 ? x0 + kSub : cx1;
-    const int y1 = y0 + kSub < cy1 ? y0 + kSub : cy1;
-    const int fw = x1 - x0, fh = y1 - y0;
-    const int L = pd.length[(size_t)f * pd.cap + cell];
-    const size_t frame_off = (size_t)f * H * W * C;
-    const T *src = in + frame_off;
-    T *dst = out + frame_off;
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
+    const int n_items = pd.counters[klass];
+    int *cursor = pd.counters + FK_NCLASS + klass;
 
-    if (L == 1) { /* blockwise.py:141-143 */
-        const int rowlen = fw * C;
-        for (int i = tid; i < fh * rowlen; i += kThreads) {
-            const int y = i / rowlen, c = i - y * rowlen;
-            const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
-            dst[o] = src[o];
+    /* claim the next non-empty item (one thread) */
+    auto fetch = [&](item_desc *d) {
+        d->valid = 0;
+        for (;;) {
+            const int idx = atomicAdd(cursor, 1);
+            if (idx >= n_items) return;
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
+            const int fw = (int)(q.z & 0xffu), fh = (int)(q.z >> 21);
+            if (fw == 0 || fh == 0) continue;
+            d->f = (int)q.x;
+            d->x0 = (int)(q.y & 0xffffu);
+            d->y0 = (int)(q.y >> 16);
+            d->fw = fw;
+            d->fh = fh;
+            d->L = (int)((q.z >> 8) & 0x1fffu);
+            d->taps_off = q.w;
+            d->valid = 1;
+            return;
         }
-        return;
-    }
-    const int r = (L - 1) >> 1;
-    const int nchunk = (L + 3) >> 2;
-    const int th = fh + 2 * r;
-    const int nseg = (fw * C + SEG - 1) / SEG;
-    const int tw = (fw + 2 * r) * C;                    /* valid tile floats per row */
-    const int twz = C * (8 * nseg + 4 + 4 * nchunk);    /* floats the H tasks may touch */
-
-    /* TMA geometry: the box origin is clamped into the image so that every clamped
-     * source row / column of this block lies inside the box. */
-    const bool xin = (x0 - r >= 0) && (x1 + r <= W);
-    const int xs_c = fast_clamp(x0 - r, 0, W - 1);
-    /* TMA needs the box to start on a 16-byte boundary of the row: fetch from the
-     * aligned-down byte and skip `skew` bytes when converting. */
-    const int c0a = (xs_c * C) & ~15;
-    const int skew = xs_c * C - c0a;
-    const int npanel = (skew + twz + 4 + kPanelB - 1) / kPanelB;
-    auto issue = [&](int rb) {
-        const int ys_c = fast_clamp(y0 - r + rb, 0, H - 1);
+    };
+    /* TMA geometry of one 32-row block of an item: the box origin is clamped into the image
+     * (so every clamped source row / column of the block lies inside the box) and moved
+     * down to a 16-byte boundary of the row, as the tensor load requires. */
+    auto issue = [&](const item_desc &d, int rb) {
+        const int r = (d.L - 1) >> 1;
+        const int nchunk = (d.L + 3) >> 2;
+        const int nseg = (d.fw * C + SEG - 1) / SEG;
+        const int twz = C * (8 * nseg + 4 + 4 * nchunk);
+        const int xs_c = fast_clamp(d.x0 - r, 0, W - 1);
+        const int c0a = (xs_c * C) & ~15;
+        const int npanel = (xs_c * C - c0a + twz + 4 + kPanelB - 1) / kPanelB;
+        const int ys_c = fast_clamp(d.y0 - r + rb, 0, H - 1);
         mbar_expect_tx(bar, (uint32_t)(npanel * kPanelBytes));
         for (int p = 0; p < npanel; p++)
-            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, f);
+            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, d.f);
     };
-    if (TMA) {
-        if (tid == 0) {
-            mbar_init(bar, 1);
-            issue(0);
-        }
-    }
 
-    {   /* taps, zero-padded; zero rows of the intermediate that padded taps may touch */
-        const float *taps = pd.taps + pd.offset[(size_t)f * pd.cap + cell];
-        for (int i = tid; i < 4 * nchunk; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
-        const int rows_touched = ((fh + kRV - 1) / kRV) * kRV + 4 + 4 * nchunk;
-        float4 *z = reinterpret_cast<float4 *>(interm + (size_t)th * IWP);
-        const int nz = (rows_touched - th) * (IWP / 4);
-        for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid == kFetchTid) {
+        if (TMA) mbar_init(bar, 1);
+        fetch(&slots[0]);
+        if (TMA && slots[0].valid && slots[0].L > 1) issue(slots[0], 0);
     }
-
-    int coff[kNQ];
-    if (TMA) {
-        if (!xin) { /* clamp-to-edge by index: tile column -> byte offset inside the box */
-            for (int j = tid; j < twz; j += kThreads) {
-                int m = -1;
-                if (j < tw) {
-                    const int px = j / C, c = j - px * C;
-                    m = skew + (fast_clamp(x0 - r + px, 0, W - 1) - xs_c) * C + c;
-                }
-                colmap[j] = m;
-            }
-        }
-        __syncthreads(); /* mbarrier init + colmap visible to all threads */
-    } else {
-        /* plain-load staging: each thread owns up to kNQ tile columns */
-#pragma unroll
-        for (int q = 0; q < kNQ; q++) {
-            const int j = tid + q * kThreads;
-            coff[q] = -2; /* not owned */
-            if (j < twz) {
-                coff[q] = -1; /* zero padding */
-                if (j < tw) {
-                    const int px = j / C, c = j - px * C;
-                    coff[q] = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
-                }
-            }
-        }
-    }
+    __syncthreads();
 
     uint32_t phase = 0;
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int rb = 0; rb < th; rb += kTB) {
-        const int nrows = th - rb < kTB ? th - rb : kTB;
+    for (int cur = 0;; cur ^= 1) {
+        const item_desc it = slots[cur];
+        if (!it.valid) break;
+        const int f = it.f, x0 = it.x0, y0 = it.y0, fw = it.fw, fh = it.fh, L = it.L;
+        const size_t frame_off = (size_t)f * H * W * C;
+        const T *src = in + frame_off;
+        T *dst = out + frame_off;
+
+        if (L == 1) { /* blockwise.py:141-143: identity fragments are copied through */
+            if (tid == kFetchTid) {
+                fetch(&slots[cur ^ 1]);
+                if (TMA && slots[cur ^ 1].valid && slots[cur ^ 1].L > 1) issue(slots[cur ^ 1], 0);
+            }
+            const int rowlen = fw * C;
+            for (int i = tid; i < fh * rowlen; i += kThreads) {
+                const int y = i / rowlen, c = i - y * rowlen;
+                const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
+                dst[o] = src[o];
+            }
+            __syncthreads();
+            continue;
+        }
+        const int r = (L - 1) >> 1;
+        const int nchunk = (L + 3) >> 2;
+        const int th = fh + 2 * r;
+        const int nseg = (fw * C + SEG - 1) / SEG;
+        const int tw = (fw + 2 * r) * C;                 /* valid tile floats per row */
+        const int twz = C * (8 * nseg + 4 + 4 * nchunk); /* floats the H tasks may touch */
+        const bool xin = (x0 - r >= 0) && (x0 + fw + r <= W);
+        const int xs_c = fast_clamp(x0 - r, 0, W - 1);
+        const int skew = xs_c * C - ((xs_c * C) & ~15);
+
+        {   /* taps, zero-padded; zero rows of the intermediate that padded taps may touch */
+            const float *taps = pd.taps + it.taps_off;
+            for (int i = tid; i < 4 * nchunk; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
+            const int rows_touched = ((fh + kRV - 1) / kRV) * kRV + 4 + 4 * nchunk;
+            float4 *z = reinterpret_cast<float4 *>(interm + (size_t)th * IWP);
+            const int nz = (rows_touched - th) * (IWP / 4);
+            for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+
+        int coff[kNQ];
         if (TMA) {
-            const int ys = y0 - r + rb;
-            const int ys_c = fast_clamp(ys, 0, H - 1);
-            mbar_wait(bar, phase);
-            phase ^= 1;
-            if (xin) {
-                /* tile word wj = raw bytes [skew + 4 wj, +4): two aligned words, funnel shift */
-                const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
-                const int wsk = skew >> 2, bsh = (skew & 3) * 8;
-                for (int row = warp; row < nrows; row += kThreads / 32) {
-                    const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
-                    const uint32_t *rp = raw32 + rr * (kPanelB / 4);
-                    float4 *tp = reinterpret_cast<float4 *>(tile + row * twp);
-                    for (int wj = lane; 4 * wj < twz; wj += 32) {
-                        const int w0 = wj + wsk, w1 = w0 + 1;
-                        const uint32_t lo = rp[(w0 >> 5) * (kPanelBytes / 4) + (w0 & 31)];
-                        const uint32_t hi = rp[(w1 >> 5) * (kPanelBytes / 4) + (w1 & 31)];
-                        tp[wj] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+            if (!xin) { /* clamp-to-edge by index: tile column -> byte offset inside the box */
+                for (int j = tid; j < twz; j += kThreads) {
+                    int m = -1;
+                    if (j < tw) {
+                        const int px = j / C, c = j - px * C;
+                        m = skew + (fast_clamp(x0 - r + px, 0, W - 1) - xs_c) * C + c;
+                        m = (m >> 7) * kPanelBytes + (m & (kPanelB - 1));
+                    }
+                    colmap[j] = m;
+                }
+                __syncthreads();
+            }
+        } else {
+            /* plain-load staging: each thread owns up to kNQ tile columns */
+#pragma unroll
+            for (int q = 0; q < kNQ; q++) {
+                const int j = tid + q * kThreads;
+                coff[q] = -2; /* not owned */
+                if (j < twz) {
+                    coff[q] = -1; /* zero padding */
+                    if (j < tw) {
+                        const int px = j / C, c = j - px * C;
+                        coff[q] = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
+                    }
+                }
+            }
+        }
+
+        for (int rb = 0; rb < th; rb += kTB) {
+            const int nrows = th - rb < kTB ? th - rb : kTB;
+            if (TMA) {
+                const int ys = y0 - r + rb;
+                const int ys_c = fast_clamp(ys, 0, H - 1);
+                mbar_wait(bar, phase);
+                phase ^= 1;
+                if (xin) {
+                    /* tile word wj = raw bytes [skew + 4 wj, +4): two aligned words and a
+                     * funnel shift; lane-constant word indices, panel steps are immediates */
+                    const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
+                    const int bsh = (skew & 3) * 8;
+                    const int w0 = lane + (skew >> 2), w1 = w0 + 1;
+                    const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
+                    const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
+                    const int nw = (twz + 3) >> 2;
+                    for (int row = warp; row < nrows; row += kThreads / 32) {
+                        const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
+                        const uint32_t *rp = raw32 + rr * (kPanelB / 4);
+                        float4 *tp = reinterpret_cast<float4 *>(tile + row * twp) + lane;
+#pragma unroll
+                        for (int p = 0; p < kMaxPanels - 1; p++) {
+                            if (lane + 32 * p < nw) {
+                                const uint32_t lo = rp[i0 + p * kPanelWords];
+                                const uint32_t hi = rp[i1 + p * kPanelWords];
+                                tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                            }
+                        }
+                    }
+                } else {
+                    for (int row = warp; row < nrows; row += kThreads / 32) {
+                        const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
+                        const unsigned char *rp = raw + rr * kPanelB;
+                        float *tp = tile + row * twp;
+                        for (int j = lane; j < twz; j += 32) {
+                            const int m = colmap[j];
+                            tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
+                        }
                     }
                 }
             } else {
-                for (int row = warp; row < nrows; row += kThreads / 32) {
-                    const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
-                    const unsigned char *rp = raw + rr * kPanelB;
-                    float *tp = tile + row * twp;
-                    for (int j = lane; j < twz; j += 32) {
-                        const int m = colmap[j];
-                        tp[j] = m >= 0
-                                    ? (float)rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))]
-                                    : 0.0f;
+                for (int row = 0; row < nrows; row++) {
+                    const int yy = fast_clamp(y0 - r + rb + row, 0, H - 1);
+                    const T *grow = src + (size_t)yy * W * C;
+                    float *trow = tile + row * twp + tid;
+#pragma unroll
+                    for (int q = 0; q < kNQ; q++) {
+                        if (coff[q] >= 0)
+                            trow[q * kThreads] = fast_px<T>::load(grow + coff[q]);
+                        else if (coff[q] == -1)
+                            trow[q * kThreads] = 0.0f;
                     }
                 }
             }
-        } else {
-            for (int row = 0; row < nrows; row++) {
-                const int yy = fast_clamp(y0 - r + rb + row, 0, H - 1);
-                const T *grow = src + (size_t)yy * W * C;
-                float *trow = tile + row * twp + tid;
+            __syncthreads();
+            /* the raw buffer is free again: fetch this item's next 32 rows during the H pass */
+            if (TMA && tid == kFetchTid && rb + kTB < th) issue(it, rb + kTB);
+            /* horizontal pass over the staged rows (blockwise.py:151) */
+            for (int task = tid; task < nrows * nseg; task += kThreads) {
+                const int row = task / nseg, seg = task - row * nseg;
+                h_task<C>(tile + row * twp + seg * SEG, wts, nchunk,
+                          interm + (size_t)(rb + row) * IWP + seg * SEG);
+            }
+            __syncthreads();
+        }
+
+        /* claim the next item and start fetching its first rows while this one finishes */
+        if (tid == kFetchTid) {
+            fetch(&slots[cur ^ 1]);
+            if (TMA && slots[cur ^ 1].valid && slots[cur ^ 1].L > 1) issue(slots[cur ^ 1], 0);
+        }
+
+        /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) ---------- */
+        const int ncg = (fw * C + 3) >> 2;
+        const int nrg = (fh + kRV - 1) / kRV;
+        const bool full = (fw * C) % 4 == 0 && fh % kRV == 0;
+        for (int task = tid; task < ncg * nrg; task += kThreads) {
+            const int rg = task / ncg, cg = task - rg * ncg;
+            float acc[kRV][4];
+            v_task(interm + (size_t)(rg * kRV) * IWP + cg * 4, IWP, wts, nchunk, acc);
+            T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
+            if (full) {
 #pragma unroll
-                for (int q = 0; q < kNQ; q++) {
-                    if (coff[q] >= 0)
-                        trow[q * kThreads] = fast_px<T>::load(grow + coff[q]);
-                    else if (coff[q] == -1)
-                        trow[q * kThreads] = 0.0f;
+                for (int j = 0; j < kRV; j++) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) orow[i] = fast_px<T>::store(acc[j][i]);
+                    orow += (size_t)W * C;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kRV; j++) {
+                    if (rg * kRV + j < fh) {
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+                            if (cg * 4 + i < fw * C) orow[i] = fast_px<T>::store(acc[j][i]);
+                    }
+                    orow += (size_t)W * C;
                 }
             }
         }
         __syncthreads();
-        if (TMA) { /* the raw buffer is free again: fetch the next 32 rows during the H pass */
-            if (tid == 0 && rb + kTB < th) issue(rb + kTB);
-        }
-        /* horizontal pass over the staged rows (blockwise.py:151) */
-        for (int task = tid; task < nrows * nseg; task += kThreads) {
-            const int row = task / nseg, seg = task - row * nseg;
-            h_task<C>(tile + row * twp + seg * SEG, wts, nchunk,
-                      interm + (size_t)(rb + row) * IWP + seg * SEG);
-        }
-        __syncthreads();
-    }
-
-    /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) ------------ */
-    const int ncg = (fw * C + 3) >> 2;
-    const int nrg = (fh + kRV - 1) / kRV;
-    for (int task = tid; task < ncg * nrg; task += kThreads) {
-        const int rg = task / ncg, cg = task - rg * ncg;
-        float acc[kRV][4];
-        v_task(interm + (size_t)(rg * kRV) * IWP + cg * 4, IWP, wts, nchunk, acc);
-#pragma unroll
-        for (int j = 0; j < kRV; j++) {
-            const int y = rg * kRV + j;
-            if (y < fh) {
-                T *orow = dst + ((size_t)(y0 + y) * W + x0) * C + cg * 4;
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-                    if (cg * 4 + i < fw * C) orow[i] = fast_px<T>::store(acc[j][i]);
-            }
-        }
     }
 }
 
@@ -443,13 +484,13 @@ struct fast_layout {
     size_t smem;
 };
 
-template <int C> fast_layout fast_layout_for(int bound_length, bool tma)
+template <int C> fast_layout fast_layout_for(int max_length, bool tma)
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG = (kSub * C + SEG - 1) / SEG;
     constexpr int IWP = NSEG * SEG + 4;
     fast_layout l;
-    const int nchunk = (bound_length + 3) / 4;
+    const int nchunk = (max_length + 3) / 4;
     l.wts_floats = 4 * nchunk;
     const int twz = C * (8 * NSEG + 4 + 4 * nchunk);
     int twp = (twz + 3) & ~3;
@@ -457,7 +498,8 @@ template <int C> fast_layout fast_layout_for(int bound_length, bool tma)
     l.twp = twp;
     l.irows = kSub + 4 + 4 * nchunk;
     l.npanel = tma ? (15 + twz + 4 + kPanelB - 1) / kPanelB : 0;
-    l.smem = (size_t)l.npanel * kPanelBytes + 16 + (tma ? (size_t)twp * sizeof(int) : 0) +
+    l.smem = (size_t)l.npanel * kPanelBytes + 16 + 2 * sizeof(item_desc) +
+             (tma ? (size_t)twp * sizeof(int) : 0) +
              ((size_t)l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
     return l;
 }
@@ -500,49 +542,53 @@ bool make_tensor_map(CUtensorMap *map, const void *in, int W, int H, int C, int 
 }
 
 template <typename T, int C, bool TMA>
-cudaError_t launch_fast(const CUtensorMap &map, const fk_plan_dev &pd, const void *in, void *out,
-                        int n_frames, int bound_length, size_t max_smem, cudaStream_t s,
-                        bool *taken)
+cudaError_t launch_fast(fk_handle *h, const CUtensorMap &map, const fk_plan_dev &pd, int klass,
+                        const void *in, void *out, int class_length, cudaStream_t s, bool *taken)
 {
-    const fast_layout l = fast_layout_for<C>(bound_length, TMA);
+    const fast_layout l = fast_layout_for<C>(class_length, TMA);
     *taken = false;
-    if (l.smem > max_smem || (!TMA && l.twp > kNQ * kThreads)) return cudaSuccess;
-    const int nsub = (pd.fragment + kSub - 1) / kSub;
-    const long long blocks = (long long)n_frames * pd.cap * nsub * nsub;
-    if (blocks > 0x7fffffffLL) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(fk_blur_fast<T, C, TMA>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l.smem);
+    const size_t max_smem = h->prop.sharedMemPerBlockOptin;
+    if (l.smem > max_smem || (!TMA && l.twp > kNQ * kThreads) || l.npanel > kMaxPanels)
+        return cudaSuccess;
+    auto kernel = fk_blur_fast<T, C, TMA>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)l.smem);
     if (e != cudaSuccess) return e;
-    fk_blur_fast<T, C, TMA><<<(unsigned)blocks, kThreads, l.smem, s>>>(
-        map, pd, (const T *)in, (T *)out, n_frames, nsub, l.wts_floats, l.twp, l.npanel);
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, l.smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaSuccess;
+    const int grid = h->prop.multiProcessorCount * occ;
+    kernel<<<grid, kThreads, l.smem, s>>>(map, pd, (const T *)in, (T *)out, klass, l.wts_floats,
+                                          l.twp, l.npanel);
     *taken = true;
     return cudaGetLastError();
 }
 
 } // namespace
 
-/* Returns cudaSuccess with *taken = false when the fast kernel cannot take the launch.
+/* Renders the items of one class list.  Returns cudaSuccess with *taken = false when the
+ * fast kernel cannot take the class (filters too long for its shared-memory layout).
  * h->variant: 0 auto, 2 = fast kernel with plain-load staging (no TMA). */
-cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
-                                int n_frames, int channels, int is_f32, int bound_length,
-                                cudaStream_t s, bool *taken)
+cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
+                                void *out, int n_frames, int channels, int is_f32,
+                                int class_length, cudaStream_t s, bool *taken)
 {
-    const size_t max_smem = h->prop.sharedMemPerBlockOptin;
     CUtensorMap map;
     memset(&map, 0, sizeof map);
     if (is_f32) {
         if (channels == 3)
-            return launch_fast<float, 3, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
-        return launch_fast<float, 1, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+            return launch_fast<float, 3, false>(h, map, pd, klass, in, out, class_length, s, taken);
+        return launch_fast<float, 1, false>(h, map, pd, klass, in, out, class_length, s, taken);
     }
     const bool tma = h->variant != 2 &&
                      make_tensor_map(&map, in, pd.width, pd.height, channels, n_frames);
     if (channels == 3) {
         if (tma)
-            return launch_fast<uint8_t, 3, true>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
-        return launch_fast<uint8_t, 3, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+            return launch_fast<uint8_t, 3, true>(h, map, pd, klass, in, out, class_length, s, taken);
+        return launch_fast<uint8_t, 3, false>(h, map, pd, klass, in, out, class_length, s, taken);
     }
     if (tma)
-        return launch_fast<uint8_t, 1, true>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
-    return launch_fast<uint8_t, 1, false>(map, pd, in, out, n_frames, bound_length, max_smem, s, taken);
+        return launch_fast<uint8_t, 1, true>(h, map, pd, klass, in, out, class_length, s, taken);
+    return launch_fast<uint8_t, 1, false>(h, map, pd, klass, in, out, class_length, s, taken);
 }

@@ -25,10 +25,44 @@ enum {
 #define FK_PLAN_THREADS 256
 #define FK_SORT_BINS 1024 /* radius bins for the descending-cost order */
 
+/*
+ * Work items.  The plan kernel turns every fragment into one or more rectangles of at most
+ * FK_RECT x FK_RECT pixels that share one filter, and appends them to one of FK_NCLASS lists
+ * by tap count, so that each list can be rendered by a kernel launch whose shared-memory
+ * layout fits its longest filter.  Inside a list, a frame's items are contiguous and ordered
+ * by descending tap count.
+ */
+#define FK_RECT 32
+#define FK_NCLASS 4
+#define FK_CLASS_L0 31  /* class 0: L <= 31 (identity fragments included) */
+#define FK_CLASS_L1 55  /* class 1: L <= 55 */
+#define FK_CLASS_L2 127 /* class 2: L <= 127; class 3: longer (generic kernel) */
+
+static __host__ __device__ __forceinline__ int fk_class_of(int L)
+{
+    return L <= FK_CLASS_L0 ? 0 : (L <= FK_CLASS_L1 ? 1 : (L <= FK_CLASS_L2 ? 2 : 3));
+}
+static inline int fk_class_lmax(int k)
+{
+    return k == 0 ? FK_CLASS_L0 : (k == 1 ? FK_CLASS_L1 : (k == 2 ? FK_CLASS_L2 : 8191));
+}
+
+/* 16 bytes, loaded as one uint4 by the render kernels. */
+struct fk_item {
+    uint32_t frame;
+    uint32_t xy;       /* x0 | y0 << 16 */
+    uint32_t geom;     /* fw | L << 8 | fh << 21   (fw <= 255, L <= 8191, fh <= 2047) */
+    uint32_t taps_off; /* offset of the L taps inside fk_plan_dev::taps */
+};
+
 /* Device-side view of a plan, passed by value to kernels. */
 struct fk_plan_dev {
     int width, height, fragment;
     int cap;             /* per-frame stride of the cell arrays */
+    int nsub;            /* rectangles per fragment axis: ceil(fragment / FK_RECT) */
+    size_t items_cap;    /* entries per class list: max_frames * cap * nsub^2 */
+    fk_item *items;      /* [FK_NCLASS][items_cap] */
+    int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors */
     double *sigma;       /* [frames][cap] */
     int32_t *raw_length; /* [frames][cap] */
     int32_t *length;     /* [frames][cap], foveal cell forced to 1 */
@@ -90,9 +124,9 @@ cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s);
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,
                            cudaStream_t s, int *launches);
-cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
-                                int n_frames, int channels, int is_f32, int bound_length,
-                                cudaStream_t s, bool *taken);
+cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
+                                void *out, int n_frames, int channels, int is_f32,
+                                int class_length, cudaStream_t s, bool *taken);
 cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s);
 
 /* Host replica of the grid geometry (tiling.py:15-28). */

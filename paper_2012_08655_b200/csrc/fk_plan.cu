@@ -51,18 +51,25 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
     return idx > n - 1 ? n - 1 : idx;
 }
 
-/* Order the cells of frame f by descending tap count (counting sort on the radius).
- * Called by all threads of the CTA that owns the frame; `length` must be visible. */
+/* Order the cells of frame f by descending tap count (counting sort on the radius) and
+ * append them, as <= FK_RECT x FK_RECT rectangles, to the per-class work lists.
+ * Called by all threads of the CTA that owns the frame; `length`, `offset` and the
+ * frame's meta words must have been written by this CTA. */
 __device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *hist /*BINS*/,
                               int *scan /*blockDim.x*/)
 {
+    __shared__ int ccount[FK_NCLASS];
+    __shared__ int cbase[FK_NCLASS];
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < FK_SORT_BINS; i += nt) hist[i] = 0;
+    if (tid < FK_NCLASS) ccount[tid] = 0;
     __syncthreads();
     const int32_t *len = pd.length + (size_t)f * pd.cap;
     for (int c = tid; c < ncells; c += nt) {
-        int r = (len[c] - 1) >> 1;
+        const int L = len[c];
+        const int r = (L - 1) >> 1;
         atomicAdd(&hist[r < FK_SORT_BINS ? r : FK_SORT_BINS - 1], 1);
+        atomicAdd(&ccount[fk_class_of(L)], 1);
     }
     __syncthreads();
     /* suffix sums: base[b] = number of cells in bins > b.  Each thread owns a run of
@@ -76,6 +83,7 @@ __device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *his
     }
     scan[tid] = local;
     __syncthreads();
+    const int nsub2 = pd.nsub * pd.nsub;
     if (tid == 0) { /* nt <= 256 partial sums: serial exclusive scan is a few hundred ns */
         int run = 0;
         for (int i = 0; i < nt; i++) {
@@ -83,6 +91,9 @@ __device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *his
             scan[i] = run;
             run += v;
         }
+        /* one reservation per class keeps a frame's items contiguous in every list */
+        for (int k = 0; k < FK_NCLASS; k++)
+            cbase[k] = ccount[k] ? atomicAdd(&pd.counters[k], ccount[k] * nsub2) : 0;
     }
     __syncthreads();
     int run = scan[tid];
@@ -100,6 +111,37 @@ __device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *his
         int r = (len[c] - 1) >> 1;
         int slot = atomicAdd(&hist[r < FK_SORT_BINS ? r : FK_SORT_BINS - 1], 1);
         order[slot] = (uint32_t)c;
+    }
+    __syncthreads();
+    /* sorted slots [0, n3) are class 3, then class 2, 1, 0 (descending tap count) */
+    const int pre[FK_NCLASS] = {ccount[3] + ccount[2] + ccount[1], ccount[3] + ccount[2],
+                                ccount[3], 0};
+    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
+    const int sx = meta[FK_META_SX], sy = meta[FK_META_SY], gw = meta[FK_META_GW];
+    const int32_t *off = pd.offset + (size_t)f * pd.cap;
+    for (int c = tid; c < ncells; c += nt) {
+        const int cell = (int)order[c];
+        const int L = len[cell];
+        const int k = fk_class_of(L);
+        const int gy = cell / gw, gx = cell - gy * gw;
+        int x0, x1, y0, y1;
+        fk_span(pd.width, pd.fragment, sx, gx, x0, x1);
+        fk_span(pd.height, pd.fragment, sy, gy, y0, y1);
+        fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + (size_t)(c - pre[k]) * nsub2;
+        for (int s = 0; s < nsub2; s++) {
+            const int sby = s / pd.nsub, sbx = s - sby * pd.nsub;
+            const int rx0 = x0 + sbx * FK_RECT, ry0 = y0 + sby * FK_RECT;
+            int fw = x1 - rx0, fh = y1 - ry0;
+            fw = fw < 0 ? 0 : (fw > FK_RECT ? FK_RECT : fw);
+            fh = fh < 0 ? 0 : (fh > FK_RECT ? FK_RECT : fh);
+            if (fw == 0 || fh == 0) fw = fh = 0; /* empty: clipped edge fragment */
+            fk_item it;
+            it.frame = (uint32_t)f;
+            it.xy = (uint32_t)rx0 | ((uint32_t)ry0 << 16);
+            it.geom = (uint32_t)fw | ((uint32_t)L << 8) | ((uint32_t)fh << 21);
+            it.taps_off = (uint32_t)off[cell];
+            dst[s] = it;
+        }
     }
 }
 
