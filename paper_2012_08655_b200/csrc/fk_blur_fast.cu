@@ -107,14 +107,16 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
-/* Four bytes of a word to four floats, exactly: PRMT into the mantissa of 2^23, FADD. */
+/* Four bytes of a word to four floats, exactly.  Two go through PRMT into the mantissa of
+ * 2^23 + FADD (ALU + FMA pipes), two through I2F.U8 with a byte selector (conversion pipe),
+ * so neither pipe is the limiter and the pass costs 6 issue slots per word. */
 __device__ __forceinline__ float4 bytes_to_float4(uint32_t w)
 {
     float4 f;
     f.x = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440)) - 8388608.0f;
-    f.y = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7441)) - 8388608.0f;
+    f.y = (float)((w >> 8) & 0xffu);
     f.z = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7442)) - 8388608.0f;
-    f.w = __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7443)) - 8388608.0f;
+    f.w = (float)(w >> 24);
     return f;
 }
 
@@ -145,12 +147,13 @@ __device__ __forceinline__ void h_task(const float *__restrict__ trow,
     }
     const float4 *nxt = src + NW / 4;
     const float4 *wp = reinterpret_cast<const float4 *>(wts);
+    float4 g4 = wp[0];
     for (int c = 0; c < nchunk; c += 3) {
 #pragma unroll
         for (int p = 0; p < 3; p++) {
             if (p > 0 && c + p >= nchunk) break;
-            const float4 g4 = wp[c + p];
             const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+            g4 = wp[c + p + 1]; /* next chunk's taps (one padding quad follows the last) */
 #pragma unroll
             for (int t = 0; t < 4; t++) {
 #pragma unroll
@@ -196,12 +199,13 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
         win[v] = *reinterpret_cast<const float4 *>(icol + (size_t)v * pitch);
     const float *nxt = icol + (size_t)12 * pitch;
     const float4 *wp = reinterpret_cast<const float4 *>(wts);
+    float4 g4 = wp[0];
     for (int c = 0; c < nchunk; c += 3) {
 #pragma unroll
         for (int p = 0; p < 3; p++) {
             if (p > 0 && c + p >= nchunk) break;
-            const float4 g4 = wp[c + p];
             const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+            g4 = wp[c + p + 1]; /* next chunk's taps */
 #pragma unroll
             for (int t = 0; t < 4; t++) {
 #pragma unroll
@@ -338,11 +342,21 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 
         {   /* taps, zero-padded; zero rows of the intermediate that padded taps may touch */
             const float *taps = pd.taps + it.taps_off;
-            for (int i = tid; i < 4 * nchunk; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
+            for (int i = tid; i < 4 * nchunk + 4; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
             const int rows_touched = ((fh + kRV - 1) / kRV) * kRV + 4 + 4 * nchunk;
             float4 *z = reinterpret_cast<float4 *>(interm + (size_t)th * IWP);
             const int nz = (rows_touched - th) * (IWP / 4);
             for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (TMA && xin) {
+                /* the converter writes whole quads up to tw only; the tile columns beyond,
+                 * which only padded taps and discarded outputs touch, are zeroed once */
+                const int q0 = (tw + 3) >> 2, nq = (twz >> 2) - q0;
+                for (int i = tid; i < nq * kTB; i += kThreads) {
+                    const int row = i / nq, q = i - row * nq;
+                    reinterpret_cast<float4 *>(tile + row * twp)[q0 + q] =
+                        make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
         }
 
         int coff[kNQ];
@@ -390,17 +404,42 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                     const int w0 = lane + (skew >> 2), w1 = w0 + 1;
                     const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
                     const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
-                    const int nw = (twz + 3) >> 2;
-                    for (int row = warp; row < nrows; row += kThreads / 32) {
-                        const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
-                        const uint32_t *rp = raw32 + rr * (kPanelB / 4);
-                        float4 *tp = reinterpret_cast<float4 *>(tile + row * twp) + lane;
+                    const int nw = (tw + 3) >> 2;
+                    bool pred[kMaxPanels - 1];
 #pragma unroll
-                        for (int p = 0; p < kMaxPanels - 1; p++) {
-                            if (lane + 32 * p < nw) {
-                                const uint32_t lo = rp[i0 + p * kPanelWords];
-                                const uint32_t hi = rp[i1 + p * kPanelWords];
-                                tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                    for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
+                    if (ys >= 0 && ys + kTB <= H) {
+                        /* no row clamping in this block: every offset is an immediate */
+                        const uint32_t *rp0 = raw32 + warp * (kPanelB / 4) + i0;
+                        const uint32_t *rp1 = raw32 + warp * (kPanelB / 4) + i1;
+                        float4 *tp = reinterpret_cast<float4 *>(tile + warp * twp) + lane;
+                        const int tstride = twp; /* 4 rows, in float4 units */
+#pragma unroll
+                        for (int i = 0; i < kTB / 4; i++) {
+                            if (warp + 4 * i < nrows) {
+#pragma unroll
+                                for (int p = 0; p < kMaxPanels - 1; p++) {
+                                    if (pred[p]) {
+                                        const uint32_t lo = rp0[i * kPanelB + p * kPanelWords];
+                                        const uint32_t hi = rp1[i * kPanelB + p * kPanelWords];
+                                        tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                    }
+                                }
+                            }
+                            tp += tstride;
+                        }
+                    } else {
+                        for (int row = warp; row < nrows; row += kThreads / 32) {
+                            const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
+                            const uint32_t *rp = raw32 + rr * (kPanelB / 4);
+                            float4 *tp = reinterpret_cast<float4 *>(tile + row * twp) + lane;
+#pragma unroll
+                            for (int p = 0; p < kMaxPanels - 1; p++) {
+                                if (pred[p]) {
+                                    const uint32_t lo = rp[i0 + p * kPanelWords];
+                                    const uint32_t hi = rp[i1 + p * kPanelWords];
+                                    tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                }
                             }
                         }
                     }
@@ -491,7 +530,7 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
     constexpr int IWP = NSEG * SEG + 4;
     fast_layout l;
     const int nchunk = (max_length + 3) / 4;
-    l.wts_floats = 4 * nchunk;
+    l.wts_floats = 4 * nchunk + 4; /* one zero quad after the last chunk (tap prefetch) */
     const int twz = C * (8 * NSEG + 4 + 4 * nchunk);
     int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
