@@ -19,10 +19,10 @@
  *               are staged with plain loads.  Tile row pitch = 4 (mod 8) floats so
  *               LDS.128 from 8 different rows hits 8 different bank groups.
  *   H pass      one task = 8 pixels x C channels of one tile row (8C accumulators).  The
- *               taps are walked in chunks of 4; the input window lives in 12C registers
- *               used as a ring with compile-time indices, refilled with LDS.128 as soon
- *               as a quad of values is dead, so the inner loop is 32C FFMA per
- *               (C + 1) LDS.128 -- the FP32 pipe, not the LSU, is the limiter.
+ *               taps are walked in chunks of 4; the input window lives in 16C registers
+ *               used as a four-slot ring with compile-time indices, one slot refilled by
+ *               LDS.128 a whole chunk before it is read, so the inner loop is 32C FFMA
+ *               per (C + 1) LDS.128 -- the FP32 pipe, not the LSU, is the limiter.
  *   V pass      one task = 8 output rows x 4 adjacent floats, same ring scheme over rows
  *               of the intermediate (128 FFMA per 5 LDS.128).
  *
@@ -130,49 +130,50 @@ __device__ __forceinline__ void h_task(const float *__restrict__ trow,
                                        const float *__restrict__ wts, int nchunk,
                                        float *__restrict__ irow)
 {
-    constexpr int NW = 12 * C; /* ring of input values */
-    constexpr int NA = 8 * C;  /* accumulators */
+    /* Ring of four slots of 4C input values.  A chunk of four taps reads slots p, p+1,
+     * p+2 (values 0 .. 11C-1 past the chunk base) and, at its start, refills slot p+3 --
+     * dead since the previous chunk -- with the values the NEXT chunk needs, so every
+     * shared-memory load has a whole chunk of FFMAs to land. */
+    constexpr int NW = 16 * C;
+    constexpr int NA = 8 * C; /* accumulators */
     float win[NW];
     float acc[NA];
 #pragma unroll
     for (int j = 0; j < NA; j++) acc[j] = 0.0f;
     const float4 *src = reinterpret_cast<const float4 *>(trow);
 #pragma unroll
-    for (int v = 0; v < NW / 4; v++) {
+    for (int v = 0; v < 3 * C; v++) {
         const float4 x = src[v];
         win[4 * v + 0] = x.x;
         win[4 * v + 1] = x.y;
         win[4 * v + 2] = x.z;
         win[4 * v + 3] = x.w;
     }
-    const float4 *nxt = src + NW / 4;
+    const float4 *nxt = src + 3 * C;
     const float4 *wp = reinterpret_cast<const float4 *>(wts);
     float4 g4 = wp[0];
-    for (int c = 0; c < nchunk; c += 3) {
+    for (int c = 0; c < nchunk; c += 4) {
 #pragma unroll
-        for (int p = 0; p < 3; p++) {
+        for (int p = 0; p < 4; p++) {
             if (p > 0 && c + p >= nchunk) break;
             const float g[4] = {g4.x, g4.y, g4.z, g4.w};
             g4 = wp[c + p + 1]; /* next chunk's taps (one padding quad follows the last) */
+#pragma unroll
+            for (int v = 0; v < C; v++) {
+                const float4 x = nxt[v];
+                const int q = (((p + 3) % 4) * C + v) * 4;
+                win[q + 0] = x.x;
+                win[q + 1] = x.y;
+                win[q + 2] = x.z;
+                win[q + 3] = x.w;
+            }
+            nxt += C;
 #pragma unroll
             for (int t = 0; t < 4; t++) {
 #pragma unroll
                 for (int j = 0; j < NA; j++)
                     acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
-                /* values below C*(t+1) of this chunk are dead: refill whole quads */
-#pragma unroll
-                for (int v = 0; v < C; v++) {
-                    if (4 * (v + 1) <= C * (t + 1) && 4 * (v + 1) > C * t) {
-                        const float4 x = nxt[v];
-                        const int q = ((p * C + v) % (3 * C)) * 4;
-                        win[q + 0] = x.x;
-                        win[q + 1] = x.y;
-                        win[q + 2] = x.z;
-                        win[q + 3] = x.w;
-                    }
-                }
             }
-            nxt += C;
         }
     }
     float4 *dst = reinterpret_cast<float4 *>(irow);
@@ -183,13 +184,13 @@ __device__ __forceinline__ void h_task(const float *__restrict__ trow,
 
 /*
  * Vertical task: acc[j][i] = sum_k g[k] * I[row0 + j + k][col0 + i], j < 8, i < 4.
- * `icol` points at I[row0][col0]; pitch in floats.
+ * `icol` points at I[row0][col0]; pitch in floats.  Same four-slot ring, over rows.
  */
 __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch,
                                        const float *__restrict__ wts, int nchunk,
                                        float (&acc)[kRV][4])
 {
-    float4 win[12];
+    float4 win[16];
 #pragma unroll
     for (int j = 0; j < kRV; j++)
 #pragma unroll
@@ -200,27 +201,28 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
     const float *nxt = icol + (size_t)12 * pitch;
     const float4 *wp = reinterpret_cast<const float4 *>(wts);
     float4 g4 = wp[0];
-    for (int c = 0; c < nchunk; c += 3) {
+    for (int c = 0; c < nchunk; c += 4) {
 #pragma unroll
-        for (int p = 0; p < 3; p++) {
+        for (int p = 0; p < 4; p++) {
             if (p > 0 && c + p >= nchunk) break;
             const float g[4] = {g4.x, g4.y, g4.z, g4.w};
             g4 = wp[c + p + 1]; /* next chunk's taps */
 #pragma unroll
+            for (int t = 0; t < 4; t++)
+                win[(4 * (p + 3) + t) % 16] =
+                    *reinterpret_cast<const float4 *>(nxt + (size_t)t * pitch);
+            nxt += (size_t)4 * pitch;
+#pragma unroll
             for (int t = 0; t < 4; t++) {
 #pragma unroll
                 for (int j = 0; j < kRV; j++) {
-                    const float4 x = win[(4 * p + t + j) % 12];
+                    const float4 x = win[(4 * p + t + j) % 16];
                     acc[j][0] = fmaf(g[t], x.x, acc[j][0]);
                     acc[j][1] = fmaf(g[t], x.y, acc[j][1]);
                     acc[j][2] = fmaf(g[t], x.z, acc[j][2]);
                     acc[j][3] = fmaf(g[t], x.w, acc[j][3]);
                 }
-                /* row t of this chunk is dead: refill its slot with the row 12 ahead */
-                win[(4 * p + t) % 12] =
-                    *reinterpret_cast<const float4 *>(nxt + (size_t)t * pitch);
             }
-            nxt += (size_t)4 * pitch;
         }
     }
 }
