@@ -411,20 +411,28 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 #pragma unroll
                     for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
                     if (ys >= 0 && ys + kTB <= H) {
-                        /* no row clamping in this block: every offset is an immediate */
+                        /* No row clamping in this block: every offset is an immediate.  The
+                         * loads are unconditional (a lane past the tile reads other shared
+                         * memory of this CTA, harmlessly) and only the stores are predicated,
+                         * so the pass is branch-free with 8 x panels independent chains per
+                         * lane.  Rows past nrows are converted too when the group of four
+                         * they belong to starts inside the block; nobody reads them. */
                         const uint32_t *rp0 = raw32 + warp * (kPanelB / 4) + i0;
                         const uint32_t *rp1 = raw32 + warp * (kPanelB / 4) + i1;
                         float4 *tp = reinterpret_cast<float4 *>(tile + warp * twp) + lane;
                         const int tstride = twp; /* 4 rows, in float4 units */
+                        const int np = (nw + 31) >> 5;
 #pragma unroll
                         for (int i = 0; i < kTB / 4; i++) {
-                            if (warp + 4 * i < nrows) {
+                            if (4 * i < nrows) {
 #pragma unroll
                                 for (int p = 0; p < kMaxPanels - 1; p++) {
-                                    if (pred[p]) {
+                                    if (p < np) { /* uniform */
                                         const uint32_t lo = rp0[i * kPanelB + p * kPanelWords];
                                         const uint32_t hi = rp1[i * kPanelB + p * kPanelWords];
-                                        tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                        const float4 v =
+                                            bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                        if (pred[p]) tp[32 * p] = v;
                                     }
                                 }
                             }
