@@ -6,18 +6,21 @@
  * (convolve.py:15).  What differs from fk_blur_generic is only how the work is laid out:
  *
  *   work items  rectangles of at most 32x32 pixels with one filter each, taken from the
- *               plan's per-class lists (fk_internal.h) by persistent CTAs of 128 threads
- *               through an atomic cursor; the launch for a class sizes its shared memory
- *               for that class's longest filter, so short filters get more CTAs per SM.
+ *               plan's per-class lists (fk_internal.h) by persistent CTAs of 128 threads,
+ *               item i of the list going to CTA i mod grid; the launch for a class sizes
+ *               its shared memory for that class's longest filter, so short filters get
+ *               more CTAs per SM.  Descriptors are prefetched two items ahead.
  *   staging     uint8 frames: the tile (rectangle + halo) is fetched 32 rows at a time by
  *               TMA (cp.async.bulk.tensor, 128-byte x 32-row boxes starting on a 16-byte
- *               boundary, zero fill outside the image) into a raw byte buffer while the
- *               previous 32 rows are being filtered, and the first block of the NEXT item
- *               is fetched during the vertical pass; a short pass converts bytes to fp32
- *               (funnel shift + PRMT + FADD) into the working tile and applies
- *               clamp-to-edge by index.  float32 frames and buffers TMA cannot describe
- *               are staged with plain loads.  Tile row pitch = 4 (mod 8) floats so
- *               LDS.128 from 8 different rows hits 8 different bank groups.
+ *               boundary, zero fill outside the image) into a raw byte buffer.  Each warp
+ *               converts ITS OWN 8 rows to fp32 (funnel shift + PRMT/FADD + I2F) into its
+ *               private rows of the working tile and then filters them, so the 32-row
+ *               blocks need no CTA-wide barrier; the last warp to leave the raw buffer
+ *               issues the TMA for the next block (or for the first block of the next
+ *               item), which lands while the H and V passes run.  float32 frames and
+ *               buffers TMA cannot describe are staged with plain loads through a column
+ *               map.  Tile row pitch = 4 (mod 8) floats so LDS.128 from 8 different rows
+ *               hits 8 different bank groups.
  *   H pass      one task = 8 pixels x C channels of one tile row (8C accumulators).  The
  *               taps are walked in chunks of 4; the input window lives in 16C registers
  *               used as a four-slot ring with compile-time indices, one slot refilled by
@@ -36,15 +39,15 @@
 namespace {
 
 constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
 constexpr int kTB = 32;        /* tile rows staged per block */
+constexpr int kWR = kTB / kWarps; /* tile rows owned by one warp: 8 */
 constexpr int kRV = 8;         /* output rows per V task */
-constexpr int kSub = FK_RECT;   /* rectangle edge */
-constexpr int kNQ = 6;         /* LDG staging: tile columns per thread (kNQ * 128 floats) */
+constexpr int kSub = FK_RECT;  /* rectangle edge */
 constexpr int kPanelB = 128;   /* TMA box: bytes per row */
 constexpr int kPanelBytes = kPanelB * kTB;
 constexpr int kPanelWords = kPanelBytes / 4;
 constexpr int kMaxPanels = 5;  /* (15 + twz + 4) / 128 for the longest fast-path filter */
-constexpr int kFetchTid = 96;  /* lane 0 of the last warp: it has no V-pass task */
 
 template <typename T> struct fast_px;
 template <> struct fast_px<uint8_t> {
@@ -227,12 +230,45 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
     }
 }
 
-/* Decoded work item, kept in shared memory (two slots: current and prefetched). */
-struct item_desc {
-    int valid;
+/* Geometry every thread derives from a 16-byte item descriptor (fk_internal.h). */
+struct item_geo {
     int f, x0, y0, fw, fh, L;
+    int r, nchunk, th, nseg, tw, twz;
+    int xs_c, skew, npanel;
+    bool xin;
     uint32_t taps_off;
 };
+
+template <int C> __device__ __forceinline__ item_geo decode_item(const uint4 q, int W)
+{
+    constexpr int SEG = 8 * C;
+    item_geo g;
+    g.f = (int)q.x;
+    g.x0 = (int)(q.y & 0xffffu);
+    g.y0 = (int)(q.y >> 16);
+    g.fw = (int)(q.z & 0xffu);
+    g.fh = (int)(q.z >> 21);
+    g.L = (int)((q.z >> 8) & 0x1fffu);
+    g.taps_off = q.w;
+    g.r = (g.L - 1) >> 1;
+    g.nchunk = (g.L + 3) >> 2;
+    g.th = g.fh + 2 * g.r;
+    g.nseg = (g.fw * C + SEG - 1) / SEG;
+    g.tw = (g.fw + 2 * g.r) * C;                  /* valid tile floats per row */
+    g.twz = C * (8 * g.nseg + 4 + 4 * g.nchunk);  /* floats the H tasks may touch */
+    g.xin = (g.x0 - g.r >= 0) && (g.x0 + g.fw + g.r <= W);
+    g.xs_c = fast_clamp(g.x0 - g.r, 0, W - 1);
+    /* TMA needs the box to start on a 16-byte boundary of the row: fetch from the
+     * aligned-down byte and skip `skew` bytes when converting */
+    g.skew = g.xs_c * C - ((g.xs_c * C) & ~15);
+    g.npanel = (g.skew + g.twz + 4 + kPanelB - 1) / kPanelB;
+    return g;
+}
+
+__device__ __forceinline__ bool item_is_blur(const uint4 q)
+{
+    return (q.z & 0xffu) != 0 && (q.z >> 21) != 0 && ((q.z >> 8) & 0x1fffu) > 1;
+}
 
 /*
  * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
@@ -249,13 +285,13 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
     constexpr int IWP = NSEG_MAX * SEG + 4;               /* pitch/4 odd: 100 or 36 */
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw panels][mbarrier 16 B][2 item slots][colmap][taps][tile][intermediate] */
+    /* layout: [raw panels][mbarrier + counter, 16 B][colmap][2 x taps][tile][intermediate] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
-    item_desc *slots = reinterpret_cast<item_desc *>(reinterpret_cast<unsigned char *>(bar) + 16);
-    int *colmap = reinterpret_cast<int *>(slots + 2);
-    float *wts = reinterpret_cast<float *>(colmap + (TMA ? twp : 0));
-    float *tile = wts + wts_floats;
+    int *raw_done = reinterpret_cast<int *>(bar + 1);
+    int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 16);
+    float *wts = reinterpret_cast<float *>(colmap + twp);
+    float *tile = wts + 2 * wts_floats;
     float *interm = tile + kTB * twp;
 
     const int W = pd.width, H = pd.height;
@@ -263,238 +299,225 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     const int warp = tid >> 5, lane = tid & 31;
     const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
     const int n_items = pd.counters[klass];
-    int *cursor = pd.counters + FK_NCLASS + klass;
-
-    /* claim the next non-empty item (one thread) */
-    auto fetch = [&](item_desc *d) {
-        d->valid = 0;
-        for (;;) {
-            const int idx = atomicAdd(cursor, 1);
-            if (idx >= n_items) return;
-            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
-            const int fw = (int)(q.z & 0xffu), fh = (int)(q.z >> 21);
-            if (fw == 0 || fh == 0) continue;
-            d->f = (int)q.x;
-            d->x0 = (int)(q.y & 0xffffu);
-            d->y0 = (int)(q.y >> 16);
-            d->fw = fw;
-            d->fh = fh;
-            d->L = (int)((q.z >> 8) & 0x1fffu);
-            d->taps_off = q.w;
-            d->valid = 1;
-            return;
-        }
-    };
-    /* TMA geometry of one 32-row block of an item: the box origin is clamped into the image
-     * (so every clamped source row / column of the block lies inside the box) and moved
-     * down to a 16-byte boundary of the row, as the tensor load requires. */
-    auto issue = [&](const item_desc &d, int rb) {
-        const int r = (d.L - 1) >> 1;
-        const int nchunk = (d.L + 3) >> 2;
-        const int nseg = (d.fw * C + SEG - 1) / SEG;
-        const int twz = C * (8 * nseg + 4 + 4 * nchunk);
-        const int xs_c = fast_clamp(d.x0 - r, 0, W - 1);
-        const int c0a = (xs_c * C) & ~15;
-        const int npanel = (xs_c * C - c0a + twz + 4 + kPanelB - 1) / kPanelB;
-        const int ys_c = fast_clamp(d.y0 - r + rb, 0, H - 1);
-        mbar_expect_tx(bar, (uint32_t)(npanel * kPanelBytes));
-        for (int p = 0; p < npanel; p++)
-            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, d.f);
+    const int stride = (int)gridDim.x;
+    const uint4 none = make_uint4(0u, 0u, 0u, 0u);
+    auto load_item = [&](int i) {
+        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
     };
 
-    if (tid == kFetchTid) {
+    /* One 32-row block of an item: the box origin is clamped into the image so that every
+     * clamped source row / column of the block lies inside the box. */
+    auto issue = [&](const item_geo &g, int rb) {
+        const int c0a = (g.xs_c * C) & ~15;
+        const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
+        mbar_expect_tx(bar, (uint32_t)(g.npanel * kPanelBytes));
+        for (int p = 0; p < g.npanel; p++)
+            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
+    };
+    /* zero-padded taps of an item into one of the two tap buffers (all threads) */
+    auto fill_taps = [&](const uint4 q, float *dst) {
+        const int L = (int)((q.z >> 8) & 0x1fffu);
+        const int n = 4 * ((L + 3) >> 2) + 4;
+        const float *taps = pd.taps + q.w;
+        for (int i = tid; i < n; i += kThreads) dst[i] = i < L ? taps[i] : 0.0f;
+    };
+
+    int idx = (int)blockIdx.x;
+    uint4 q_cur = load_item(idx);
+    uint4 q_nxt = load_item(idx + stride);
+    if (tid == 0) {
         if (TMA) mbar_init(bar, 1);
-        fetch(&slots[0]);
-        if (TMA && slots[0].valid && slots[0].L > 1) issue(slots[0], 0);
+        *raw_done = 0;
     }
+    if (item_is_blur(q_cur)) fill_taps(q_cur, wts);
     __syncthreads();
+    if (TMA && tid == 0 && item_is_blur(q_cur)) issue(decode_item<C>(q_cur, W), 0);
 
     uint32_t phase = 0;
-    for (int cur = 0;; cur ^= 1) {
-        const item_desc it = slots[cur];
-        if (!it.valid) break;
-        const int f = it.f, x0 = it.x0, y0 = it.y0, fw = it.fw, fh = it.fh, L = it.L;
-        const size_t frame_off = (size_t)f * H * W * C;
-        const T *src = in + frame_off;
-        T *dst = out + frame_off;
+    int wsel = 0;
+    uint4 q_nn = none;
+    for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wsel ^= 1) {
+        q_nn = load_item(idx + 2 * stride); /* descriptor prefetch, two items ahead */
+        float *w_cur = wts + wsel * wts_floats;
+        float *w_nxt = wts + (wsel ^ 1) * wts_floats;
+        const bool next_blur = item_is_blur(q_nxt);
+        /* every item prepares its successor's taps; they become visible at the barrier
+         * that ends this item (the buffer was last read two items ago) */
+        if (next_blur) fill_taps(q_nxt, w_nxt);
 
-        if (L == 1) { /* blockwise.py:141-143: identity fragments are copied through */
-            if (tid == kFetchTid) {
-                fetch(&slots[cur ^ 1]);
-                if (TMA && slots[cur ^ 1].valid && slots[cur ^ 1].L > 1) issue(slots[cur ^ 1], 0);
+        if (!item_is_blur(q_cur)) {
+            const item_geo g = decode_item<C>(q_cur, W);
+            if (g.fw != 0 && g.fh != 0) { /* blockwise.py:141-143: identity fragments */
+                const size_t frame_off = (size_t)g.f * H * W * C;
+                const int rowlen = g.fw * C;
+                for (int i = tid; i < g.fh * rowlen; i += kThreads) {
+                    const int y = i / rowlen, c = i - y * rowlen;
+                    const size_t o = frame_off + ((size_t)(g.y0 + y) * W + g.x0) * C + c;
+                    out[o] = in[o];
+                }
             }
-            const int rowlen = fw * C;
-            for (int i = tid; i < fh * rowlen; i += kThreads) {
-                const int y = i / rowlen, c = i - y * rowlen;
-                const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
-                dst[o] = src[o];
-            }
+            /* all warps are aligned here and the raw buffer is idle */
+            if (TMA && tid == 0 && next_blur) issue(decode_item<C>(q_nxt, W), 0);
             __syncthreads();
             continue;
         }
-        const int r = (L - 1) >> 1;
-        const int nchunk = (L + 3) >> 2;
-        const int th = fh + 2 * r;
-        const int nseg = (fw * C + SEG - 1) / SEG;
-        const int tw = (fw + 2 * r) * C;                 /* valid tile floats per row */
-        const int twz = C * (8 * nseg + 4 + 4 * nchunk); /* floats the H tasks may touch */
-        const bool xin = (x0 - r >= 0) && (x0 + fw + r <= W);
-        const int xs_c = fast_clamp(x0 - r, 0, W - 1);
-        const int skew = xs_c * C - ((xs_c * C) & ~15);
 
-        {   /* taps, zero-padded; zero rows of the intermediate that padded taps may touch */
-            const float *taps = pd.taps + it.taps_off;
-            for (int i = tid; i < 4 * nchunk + 4; i += kThreads) wts[i] = i < L ? taps[i] : 0.0f;
+        const item_geo g = decode_item<C>(q_cur, W);
+        const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
+        const int nchunk = g.nchunk, th = g.th, nseg = g.nseg, tw = g.tw, twz = g.twz;
+        const size_t frame_off = (size_t)g.f * H * W * C;
+        const T *src = in + frame_off;
+        T *dst = out + frame_off;
+        const bool vec = TMA && g.xin; /* vector converter, no column map */
+
+        {   /* zero the rows of the intermediate that only padded taps touch */
             const int rows_touched = ((fh + kRV - 1) / kRV) * kRV + 4 + 4 * nchunk;
             float4 *z = reinterpret_cast<float4 *>(interm + (size_t)th * IWP);
             const int nz = (rows_touched - th) * (IWP / 4);
             for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (TMA && xin) {
-                /* the converter writes whole quads up to tw only; the tile columns beyond,
-                 * which only padded taps and discarded outputs touch, are zeroed once */
-                const int q0 = (tw + 3) >> 2, nq = (twz >> 2) - q0;
-                for (int i = tid; i < nq * kTB; i += kThreads) {
-                    const int row = i / nq, q = i - row * nq;
-                    reinterpret_cast<float4 *>(tile + row * twp)[q0 + q] =
-                        make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
         }
-
-        int coff[kNQ];
-        if (TMA) {
-            if (!xin) { /* clamp-to-edge by index: tile column -> byte offset inside the box */
-                for (int j = tid; j < twz; j += kThreads) {
-                    int m = -1;
-                    if (j < tw) {
-                        const int px = j / C, c = j - px * C;
-                        m = skew + (fast_clamp(x0 - r + px, 0, W - 1) - xs_c) * C + c;
-                        m = (m >> 7) * kPanelBytes + (m & (kPanelB - 1));
-                    }
-                    colmap[j] = m;
-                }
-                __syncthreads();
+        if (vec) {
+            /* the vector converter writes whole quads up to tw only; the tile columns
+             * beyond, which only padded taps and discarded outputs touch, are zeroed
+             * once per item by the warp that owns the rows */
+            const int q0 = (tw + 3) >> 2, nq = (twz >> 2) - q0;
+            for (int i = lane; i < nq * kWR; i += 32) {
+                const int row = i / nq, q = i - row * nq;
+                reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[q0 + q] =
+                    make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            __syncwarp();
         } else {
-            /* plain-load staging: each thread owns up to kNQ tile columns */
-#pragma unroll
-            for (int q = 0; q < kNQ; q++) {
-                const int j = tid + q * kThreads;
-                coff[q] = -2; /* not owned */
-                if (j < twz) {
-                    coff[q] = -1; /* zero padding */
-                    if (j < tw) {
-                        const int px = j / C, c = j - px * C;
-                        coff[q] = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
+            /* clamp-to-edge by index.  TMA: tile column -> byte offset inside the box;
+             * plain loads: tile column -> element offset inside the image row */
+            for (int j = tid; j < twz; j += kThreads) {
+                int m = -1;
+                if (j < tw) {
+                    const int px = j / C, c = j - px * C;
+                    const int xx = fast_clamp(x0 - r + px, 0, W - 1);
+                    if (TMA) {
+                        m = g.skew + (xx - g.xs_c) * C + c;
+                        m = (m >> 7) * kPanelBytes + (m & (kPanelB - 1));
+                    } else {
+                        m = xx * C + c;
                     }
                 }
+                colmap[j] = m;
             }
+            __syncthreads();
         }
 
         for (int rb = 0; rb < th; rb += kTB) {
             const int nrows = th - rb < kTB ? th - rb : kTB;
+            const int ys = y0 - r + rb;
+            const bool mine = warp * kWR < nrows; /* this warp owns rows of this block */
             if (TMA) {
-                const int ys = y0 - r + rb;
-                const int ys_c = fast_clamp(ys, 0, H - 1);
                 mbar_wait(bar, phase);
                 phase ^= 1;
-                if (xin) {
-                    /* tile word wj = raw bytes [skew + 4 wj, +4): two aligned words and a
-                     * funnel shift; lane-constant word indices, panel steps are immediates */
-                    const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
-                    const int bsh = (skew & 3) * 8;
-                    const int w0 = lane + (skew >> 2), w1 = w0 + 1;
-                    const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
-                    const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
-                    const int nw = (tw + 3) >> 2;
-                    bool pred[kMaxPanels - 1];
-#pragma unroll
-                    for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
-                    if (ys >= 0 && ys + kTB <= H) {
-                        /* No row clamping in this block: every offset is an immediate.  The
-                         * loads are unconditional (a lane past the tile reads other shared
-                         * memory of this CTA, harmlessly) and only the stores are predicated,
-                         * so the pass is branch-free with 8 x panels independent chains per
-                         * lane.  Rows past nrows are converted too when the group of four
-                         * they belong to starts inside the block; nobody reads them. */
-                        const uint32_t *rp0 = raw32 + warp * (kPanelB / 4) + i0;
-                        const uint32_t *rp1 = raw32 + warp * (kPanelB / 4) + i1;
-                        float4 *tp = reinterpret_cast<float4 *>(tile + warp * twp) + lane;
-                        const int tstride = twp; /* 4 rows, in float4 units */
+                if (mine) {
+                    const int ys_c = fast_clamp(ys, 0, H - 1);
+                    if (vec) {
+                        /* tile word wj = raw bytes [skew + 4 wj, +4): two aligned words and
+                         * a funnel shift; lane-constant indices, row and panel steps are
+                         * immediates.  Loads are unconditional (a lane past the tile reads
+                         * other shared memory of this CTA, harmlessly), stores predicated:
+                         * branch-free, 8 x panels independent chains per lane. */
+                        const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
+                        const int bsh = (g.skew & 3) * 8;
+                        const int w0 = lane + (g.skew >> 2), w1 = w0 + 1;
+                        const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
+                        const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
+                        const int nw = (tw + 3) >> 2;
                         const int np = (nw + 31) >> 5;
+                        bool pred[kMaxPanels - 1];
 #pragma unroll
-                        for (int i = 0; i < kTB / 4; i++) {
-                            if (4 * i < nrows) {
+                        for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
+                        float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp) + lane;
+                        if (ys >= 0 && ys + kTB <= H) {
+                            const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
+                            const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
+#pragma unroll
+                            for (int i = 0; i < kWR; i++) {
 #pragma unroll
                                 for (int p = 0; p < kMaxPanels - 1; p++) {
                                     if (p < np) { /* uniform */
-                                        const uint32_t lo = rp0[i * kPanelB + p * kPanelWords];
-                                        const uint32_t hi = rp1[i * kPanelB + p * kPanelWords];
+                                        const uint32_t lo = rp0[i * (kPanelB / 4) + p * kPanelWords];
+                                        const uint32_t hi = rp1[i * (kPanelB / 4) + p * kPanelWords];
                                         const float4 v =
                                             bytes_to_float4(__funnelshift_r(lo, hi, bsh));
                                         if (pred[p]) tp[32 * p] = v;
                                     }
                                 }
+                                tp += twp / 4;
                             }
-                            tp += tstride;
+                        } else { /* rows clamp at the top / bottom edge of the image */
+                            for (int i = 0; i < kWR; i++) {
+                                const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
+                                const uint32_t *rp = raw32 + rr * (kPanelB / 4);
+#pragma unroll
+                                for (int p = 0; p < kMaxPanels - 1; p++) {
+                                    if (pred[p]) {
+                                        const uint32_t lo = rp[i0 + p * kPanelWords];
+                                        const uint32_t hi = rp[i1 + p * kPanelWords];
+                                        tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                    }
+                                }
+                                tp += twp / 4;
+                            }
                         }
                     } else {
-                        for (int row = warp; row < nrows; row += kThreads / 32) {
-                            const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
-                            const uint32_t *rp = raw32 + rr * (kPanelB / 4);
-                            float4 *tp = reinterpret_cast<float4 *>(tile + row * twp) + lane;
-#pragma unroll
-                            for (int p = 0; p < kMaxPanels - 1; p++) {
-                                if (pred[p]) {
-                                    const uint32_t lo = rp[i0 + p * kPanelWords];
-                                    const uint32_t hi = rp[i1 + p * kPanelWords];
-                                    tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
-                                }
+                        for (int i = 0; i < kWR; i++) {
+                            const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
+                            const unsigned char *rp = raw + rr * kPanelB;
+                            float *tp = tile + (warp * kWR + i) * twp;
+                            for (int j = lane; j < twz; j += 32) {
+                                const int m = colmap[j];
+                                tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
                             }
                         }
                     }
-                } else {
-                    for (int row = warp; row < nrows; row += kThreads / 32) {
-                        const int rr = fast_clamp(ys + row, 0, H - 1) - ys_c;
-                        const unsigned char *rp = raw + rr * kPanelB;
-                        float *tp = tile + row * twp;
-                        for (int j = lane; j < twz; j += 32) {
-                            const int m = colmap[j];
-                            tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
-                        }
+                }
+                __syncwarp();
+                /* this warp is done with the raw bytes; the last one out refills them with
+                 * the next 32 rows, or with the first rows of the next item */
+                if (lane == 0) {
+                    if (atomicAdd(raw_done, 1) == kWarps - 1) {
+                        *raw_done = 0;
+                        if (rb + kTB < th)
+                            issue(g, rb + kTB);
+                        else if (next_blur)
+                            issue(decode_item<C>(q_nxt, W), 0);
                     }
                 }
-            } else {
-                for (int row = 0; row < nrows; row++) {
-                    const int yy = fast_clamp(y0 - r + rb + row, 0, H - 1);
-                    const T *grow = src + (size_t)yy * W * C;
-                    float *trow = tile + row * twp + tid;
+            } else if (mine) {
+                /* plain loads, eight rows in flight per lane */
+                const T *grow[kWR];
 #pragma unroll
-                    for (int q = 0; q < kNQ; q++) {
-                        if (coff[q] >= 0)
-                            trow[q * kThreads] = fast_px<T>::load(grow + coff[q]);
-                        else if (coff[q] == -1)
-                            trow[q * kThreads] = 0.0f;
-                    }
+                for (int i = 0; i < kWR; i++)
+                    grow[i] = src + (size_t)fast_clamp(ys + warp * kWR + i, 0, H - 1) * W * C;
+                float *tp = tile + warp * kWR * twp;
+                for (int j = lane; j < twz; j += 32) {
+                    const int m = colmap[j];
+                    float v[kWR];
+#pragma unroll
+                    for (int i = 0; i < kWR; i++) v[i] = m >= 0 ? fast_px<T>::load(grow[i] + m) : 0.0f;
+#pragma unroll
+                    for (int i = 0; i < kWR; i++) tp[i * twp + j] = v[i];
+                }
+                __syncwarp();
+            }
+            /* horizontal pass over this warp's rows (blockwise.py:151) */
+            if (mine) {
+                for (int task = lane; task < kWR * nseg; task += 32) {
+                    const int row = warp * kWR + task / nseg, seg = task % nseg;
+                    if (row < nrows)
+                        h_task<C>(tile + row * twp + seg * SEG, w_cur, nchunk,
+                                  interm + (size_t)(rb + row) * IWP + seg * SEG);
                 }
             }
-            __syncthreads();
-            /* the raw buffer is free again: fetch this item's next 32 rows during the H pass */
-            if (TMA && tid == kFetchTid && rb + kTB < th) issue(it, rb + kTB);
-            /* horizontal pass over the staged rows (blockwise.py:151) */
-            for (int task = tid; task < nrows * nseg; task += kThreads) {
-                const int row = task / nseg, seg = task - row * nseg;
-                h_task<C>(tile + row * twp + seg * SEG, wts, nchunk,
-                          interm + (size_t)(rb + row) * IWP + seg * SEG);
-            }
-            __syncthreads();
+            __syncwarp(); /* the next block's conversion overwrites this warp's tile rows */
         }
-
-        /* claim the next item and start fetching its first rows while this one finishes */
-        if (tid == kFetchTid) {
-            fetch(&slots[cur ^ 1]);
-            if (TMA && slots[cur ^ 1].valid && slots[cur ^ 1].L > 1) issue(slots[cur ^ 1], 0);
-        }
+        __syncthreads(); /* the whole intermediate is written */
 
         /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) ---------- */
         const int ncg = (fw * C + 3) >> 2;
@@ -503,7 +526,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         for (int task = tid; task < ncg * nrg; task += kThreads) {
             const int rg = task / ncg, cg = task - rg * ncg;
             float acc[kRV][4];
-            v_task(interm + (size_t)(rg * kRV) * IWP + cg * 4, IWP, wts, nchunk, acc);
+            v_task(interm + (size_t)(rg * kRV) * IWP + cg * 4, IWP, w_cur, nchunk, acc);
             T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
             if (full) {
 #pragma unroll
@@ -524,7 +547,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
             }
         }
-        __syncthreads();
+        __syncthreads(); /* intermediate, taps and column map are free for the next item */
     }
 }
 
@@ -547,9 +570,8 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
     l.twp = twp;
     l.irows = kSub + 4 + 4 * nchunk;
     l.npanel = tma ? (15 + twz + 4 + kPanelB - 1) / kPanelB : 0;
-    l.smem = (size_t)l.npanel * kPanelBytes + 16 + 2 * sizeof(item_desc) +
-             (tma ? (size_t)twp * sizeof(int) : 0) +
-             ((size_t)l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
+    l.smem = (size_t)l.npanel * kPanelBytes + 16 + (size_t)twp * sizeof(int) +
+             ((size_t)2 * l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
     return l;
 }
 
@@ -597,8 +619,7 @@ cudaError_t launch_fast(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     const fast_layout l = fast_layout_for<C>(class_length, TMA);
     *taken = false;
     const size_t max_smem = h->prop.sharedMemPerBlockOptin;
-    if (l.smem > max_smem || (!TMA && l.twp > kNQ * kThreads) || l.npanel > kMaxPanels)
-        return cudaSuccess;
+    if (l.smem > max_smem || (TMA && l.npanel > kMaxPanels)) return cudaSuccess;
     auto kernel = fk_blur_fast<T, C, TMA>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)l.smem);
