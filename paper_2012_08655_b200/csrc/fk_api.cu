@@ -246,8 +246,9 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     d.height = height;
     d.fragment = fragment_size;
     d.cap = gwm * ghm;
-    d.nsub = (fragment_size + FK_RECT - 1) / FK_RECT;
-    d.items_cap = (size_t)max_frames * d.cap * d.nsub * d.nsub;
+    d.nsub_x = (fragment_size + FK_RECT - 1) / FK_RECT;
+    d.nsub_y = (fragment_size + FK_STRIP_ROWS - 1) / FK_STRIP_ROWS;
+    d.items_cap = (size_t)max_frames * d.cap * d.nsub_x * d.nsub_y;
     if ((double)d.items_cap > 2.0e9) {
         delete p;
         return fk_fail(h, FK_EINVAL, "batch too large: %d frames x %d fragments", max_frames, d.cap);
@@ -258,7 +259,6 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     if (e == cudaSuccess) e = cudaMalloc(&d.raw_length, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.length, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.offset, cells * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&d.order, cells * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.items, FK_NCLASS * d.items_cap * sizeof(fk_item));
     if (e == cudaSuccess) e = cudaMalloc(&d.counters, 2 * FK_NCLASS * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.meta, (size_t)max_frames * FK_META_WORDS * sizeof(int32_t));
@@ -280,7 +280,6 @@ int fk_plan_destroy(fk_plan *p)
     cudaFree(p->d.raw_length);
     cudaFree(p->d.length);
     cudaFree(p->d.offset);
-    cudaFree(p->d.order);
     cudaFree(p->d.items);
     cudaFree(p->d.counters);
     cudaFree(p->d.meta);

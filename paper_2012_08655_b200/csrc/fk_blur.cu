@@ -66,10 +66,10 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
         const int idx = s_idx;
         if (idx >= n_items) break;
         const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
-        const int fw = (int)(q.z & 0xffu), fh = (int)(q.z >> 21);
-        if (fw == 0 || fh == 0) continue;
+        const int fw = (int)(q.z & 0xffu), fh_all = (int)(q.z >> 21);
+        if (fw == 0 || fh_all == 0) continue;
         const int f = (int)q.x;
-        const int x0 = (int)(q.y & 0xffffu), y0 = (int)(q.y >> 16);
+        const int x0 = (int)(q.y & 0xffffu), y0_all = (int)(q.y >> 16);
         const int x1 = x0 + fw;
         const int L = (int)((q.z >> 8) & 0x1fffu);
         const size_t frame_off = (size_t)f * H * W * C;
@@ -78,9 +78,9 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
 
         if (L == 1) { /* blockwise.py:141-143: identity fragments are copied through */
             const int rowlen = fw * C;
-            for (int i = tid; i < fh * rowlen; i += nt) {
+            for (int i = tid; i < fh_all * rowlen; i += nt) {
                 const int y = i / rowlen, c = i - y * rowlen;
-                const size_t o = ((size_t)(y0 + y) * W + x0) * C + c;
+                const size_t o = ((size_t)(y0_all + y) * W + x0) * C + c;
                 dst[o] = src[o];
             }
             continue;
@@ -89,11 +89,14 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
         const float *taps = pd.taps + q.w;
         for (int i = tid; i < L; i += nt) wts[i] = taps[i];
 
+        __syncthreads();
+        /* a strip is rendered FK_RECT rows at a time (the intermediate is sized for that) */
+        for (int y0 = y0_all; y0 < y0_all + fh_all; y0 += FK_RECT) {
+        const int fh = y0_all + fh_all - y0 < FK_RECT ? y0_all + fh_all - y0 : FK_RECT;
         const int th = fh + 2 * r;
         int ws = interm_floats / (th * C);
         ws = ws > fw ? fw : ws;
-        if (ws < 1) continue; /* host sizes the buffer so that this cannot happen */
-        __syncthreads();
+        if (ws < 1) break; /* host sizes the buffer so that this cannot happen */
 
         for (int xs = x0; xs < x1; xs += ws) {
             const int sw = (x1 - xs) < ws ? (x1 - xs) : ws;
@@ -122,6 +125,7 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
                 dst[((size_t)(y0 + y) * W + xs) * C + col] = fk_px<T>::store(acc);
             }
             __syncthreads();
+        }
         }
     }
 }

@@ -5,8 +5,10 @@
  * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
  * (convolve.py:15).  What differs from fk_blur_generic is only how the work is laid out:
  *
- *   work items  rectangles of at most 32x32 pixels with one filter each, taken from the
- *               plan's per-class lists (fk_internal.h) by persistent CTAs of 128 threads,
+ *   work items  strips at most 32 pixels wide and 128 tall with one filter each (vertical
+ *               runs of same-filter fragments share the horizontal pass over the halo rows
+ *               between them), taken from the plan's per-class lists (fk_internal.h) by
+ *               persistent CTAs of 128 threads,
  *               item i of the list going to CTA i mod grid; the launch for a class sizes
  *               its shared memory for that class's longest filter, so short filters get
  *               more CTAs per SM.  Descriptors are prefetched two items ahead.
@@ -27,7 +29,10 @@
  *               LDS.128 a whole chunk before it is read, so the inner loop is 32C FFMA
  *               per (C + 1) LDS.128 -- the FP32 pipe, not the LSU, is the limiter.
  *   V pass      one task = 8 output rows x 4 adjacent floats, same ring scheme over rows
- *               of the intermediate (128 FFMA per 5 LDS.128).
+ *               of the intermediate (128 FFMA per 5 LDS.128).  The intermediate itself is
+ *               a ring of 2r + 40 rows in shared memory: after each 32-row block the
+ *               output groups whose 8 + 2r rows are complete are rendered, so a strip of
+ *               any height needs no more shared memory than a single fragment.
  *
  * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can
  * touch holds a finite value so 0 * garbage never produces a NaN.
@@ -189,19 +194,27 @@ __device__ __forceinline__ void h_task(const float *__restrict__ trow,
  * Vertical task: acc[j][i] = sum_k g[k] * I[row0 + j + k][col0 + i], j < 8, i < 4.
  * `icol` points at I[row0][col0]; pitch in floats.  Same four-slot ring, over rows.
  */
-__device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch,
-                                       const float *__restrict__ wts, int nchunk,
+__device__ __forceinline__ void v_task(const float *__restrict__ ring, int pitch, int row0,
+                                       int cap, const float *__restrict__ wts, int nchunk,
                                        float (&acc)[kRV][4])
 {
+    /* `ring` points at column col0 of row 0 of the intermediate ring buffer of `cap` rows;
+     * row0 and cap are multiples of 4, so a group of four rows never straddles the wrap */
     float4 win[16];
 #pragma unroll
     for (int j = 0; j < kRV; j++)
 #pragma unroll
         for (int i = 0; i < 4; i++) acc[j][i] = 0.0f;
+    int rp = row0;
 #pragma unroll
-    for (int v = 0; v < 12; v++)
-        win[v] = *reinterpret_cast<const float4 *>(icol + (size_t)v * pitch);
-    const float *nxt = icol + (size_t)12 * pitch;
+    for (int v = 0; v < 3; v++) {
+        const float *base = ring + (size_t)rp * pitch;
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+            win[4 * v + t] = *reinterpret_cast<const float4 *>(base + (size_t)t * pitch);
+        rp += 4;
+        rp = rp >= cap ? rp - cap : rp;
+    }
     const float4 *wp = reinterpret_cast<const float4 *>(wts);
     float4 g4 = wp[0];
     for (int c = 0; c < nchunk; c += 4) {
@@ -210,11 +223,13 @@ __device__ __forceinline__ void v_task(const float *__restrict__ icol, int pitch
             if (p > 0 && c + p >= nchunk) break;
             const float g[4] = {g4.x, g4.y, g4.z, g4.w};
             g4 = wp[c + p + 1]; /* next chunk's taps */
+            const float *nxt = ring + (size_t)rp * pitch;
 #pragma unroll
             for (int t = 0; t < 4; t++)
                 win[(4 * (p + 3) + t) % 16] =
                     *reinterpret_cast<const float4 *>(nxt + (size_t)t * pitch);
-            nxt += (size_t)4 * pitch;
+            rp += 4;
+            rp = rp >= cap ? rp - cap : rp;
 #pragma unroll
             for (int t = 0; t < 4; t++) {
 #pragma unroll
@@ -279,7 +294,7 @@ template <typename T, int C, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
 fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
              const T *__restrict__ in, T *__restrict__ out, int klass, int wts_floats, int twp,
-             int npanel_max)
+             int npanel_max, int icap)
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
@@ -329,6 +344,10 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         if (TMA) mbar_init(bar, 1);
         *raw_done = 0;
     }
+    /* the intermediate is a ring of icap rows; rows a padded tap can reach before they
+     * have been produced must hold finite values, so start from zeros */
+    for (int i = tid; i < icap * (IWP / 4); i += kThreads)
+        reinterpret_cast<float4 *>(interm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (item_is_blur(q_cur)) fill_taps(q_cur, wts);
     __syncthreads();
     if (TMA && tid == 0 && item_is_blur(q_cur)) issue(decode_item<C>(q_cur, W), 0);
@@ -370,12 +389,6 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         T *dst = out + frame_off;
         const bool vec = TMA && g.xin; /* vector converter, no column map */
 
-        {   /* zero the rows of the intermediate that only padded taps touch */
-            const int rows_touched = ((fh + kRV - 1) / kRV) * kRV + 4 + 4 * nchunk;
-            float4 *z = reinterpret_cast<float4 *>(interm + (size_t)th * IWP);
-            const int nz = (rows_touched - th) * (IWP / 4);
-            for (int i = tid; i < nz; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
         if (vec) {
             /* the vector converter writes whole quads up to tw only; the tile columns
              * beyond, which only padded taps and discarded outputs touch, are zeroed
@@ -407,6 +420,10 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             __syncthreads();
         }
 
+        const int ngroups = (fh + kRV - 1) / kRV; /* groups of 8 output rows */
+        const int ncg = (fw * C + 3) >> 2;        /* quads of output floats per row */
+        const bool wide = (fw * C) % 4 == 0;
+        int jdone = 0, rbm = 0;                   /* groups rendered; rb mod icap */
         for (int rb = 0; rb < th; rb += kTB) {
             const int nrows = th - rb < kTB ? th - rb : kTB;
             const int ys = y0 - r + rb;
@@ -506,48 +523,64 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
                 __syncwarp();
             }
-            /* horizontal pass over this warp's rows (blockwise.py:151) */
+            /* horizontal pass over this warp's rows (blockwise.py:151) into the ring */
             if (mine) {
                 for (int task = lane; task < kWR * nseg; task += 32) {
                     const int row = warp * kWR + task / nseg, seg = task % nseg;
-                    if (row < nrows)
+                    if (row < nrows) {
+                        int rr = rbm + row;
+                        rr = rr >= icap ? rr - icap : rr;
                         h_task<C>(tile + row * twp + seg * SEG, w_cur, nchunk,
-                                  interm + (size_t)(rb + row) * IWP + seg * SEG);
+                                  interm + (size_t)rr * IWP + seg * SEG);
+                    }
                 }
             }
             __syncwarp(); /* the next block's conversion overwrites this warp's tile rows */
-        }
-        __syncthreads(); /* the whole intermediate is written */
+            rbm += kTB;
+            rbm = rbm >= icap ? rbm - icap : rbm;
 
-        /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) ---------- */
-        const int ncg = (fw * C + 3) >> 2;
-        const int nrg = (fh + kRV - 1) / kRV;
-        const bool full = (fw * C) % 4 == 0 && fh % kRV == 0;
-        for (int task = tid; task < ncg * nrg; task += kThreads) {
-            const int rg = task / ncg, cg = task - rg * ncg;
-            float acc[kRV][4];
-            v_task(interm + (size_t)(rg * kRV) * IWP + cg * 4, IWP, w_cur, nchunk, acc);
-            T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
-            if (full) {
+            /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) over the
+             * groups of 8 output rows whose 8 + 2r intermediate rows are all there ------ */
+            const int produced = rb + nrows;
+            int jend = ngroups;
+            if (produced < th) {
+                const int avail = produced - 2 * r - kRV;
+                jend = avail >= 0 ? avail / kRV + 1 : 0;
+                jend = jend < ngroups ? jend : ngroups;
+            }
+            if (jend > jdone) { /* uniform across the CTA */
+                __syncthreads(); /* every warp's rows of this block are in the ring */
+                const int ntask = (jend - jdone) * ncg;
+                for (int task = tid; task < ntask; task += kThreads) {
+                    const int rg = jdone + task / ncg, cg = task % ncg;
+                    float acc[kRV][4];
+                    v_task(interm + cg * 4, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
+                    T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
+                    if (wide && rg * kRV + kRV <= fh) {
 #pragma unroll
-                for (int j = 0; j < kRV; j++) {
+                        for (int j = 0; j < kRV; j++) {
 #pragma unroll
-                    for (int i = 0; i < 4; i++) orow[i] = fast_px<T>::store(acc[j][i]);
-                    orow += (size_t)W * C;
-                }
-            } else {
+                            for (int i = 0; i < 4; i++) orow[i] = fast_px<T>::store(acc[j][i]);
+                            orow += (size_t)W * C;
+                        }
+                    } else {
 #pragma unroll
-                for (int j = 0; j < kRV; j++) {
-                    if (rg * kRV + j < fh) {
+                        for (int j = 0; j < kRV; j++) {
+                            if (rg * kRV + j < fh) {
 #pragma unroll
-                        for (int i = 0; i < 4; i++)
-                            if (cg * 4 + i < fw * C) orow[i] = fast_px<T>::store(acc[j][i]);
+                                for (int i = 0; i < 4; i++)
+                                    if (cg * 4 + i < fw * C) orow[i] = fast_px<T>::store(acc[j][i]);
+                            }
+                            orow += (size_t)W * C;
+                        }
                     }
-                    orow += (size_t)W * C;
                 }
+                jdone = jend;
+                /* the next block overwrites ring rows these groups were reading; after the
+                 * last block this also frees taps and column map for the next item */
+                __syncthreads();
             }
         }
-        __syncthreads(); /* intermediate, taps and column map are free for the next item */
     }
 }
 
@@ -568,7 +601,9 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
     int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
-    l.irows = kSub + 4 + 4 * nchunk;
+    /* ring of intermediate rows: 2r + 40 lets a block of 32 new rows be written while the
+     * rows the pending output groups still need stay intact (multiple of 4) */
+    l.irows = (2 * ((max_length - 1) / 2) + 40 + 3) & ~3;
     l.npanel = tma ? (15 + twz + 4 + kPanelB - 1) / kPanelB : 0;
     l.smem = (size_t)l.npanel * kPanelBytes + 16 + (size_t)twp * sizeof(int) +
              ((size_t)2 * l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
@@ -630,7 +665,7 @@ cudaError_t launch_fast(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     if (occ < 1) return cudaSuccess;
     const int grid = h->prop.multiProcessorCount * occ;
     kernel<<<grid, kThreads, l.smem, s>>>(map, pd, (const T *)in, (T *)out, klass, l.wts_floats,
-                                          l.twp, l.npanel);
+                                          l.twp, l.npanel, l.irows);
     *taken = true;
     return cudaGetLastError();
 }

@@ -23,16 +23,18 @@ enum {
 
 #define FK_LUT_DEFAULT_MAX 255
 #define FK_PLAN_THREADS 256
-#define FK_SORT_BINS 1024 /* radius bins for the descending-cost order */
 
 /*
- * Work items.  The plan kernel turns every fragment into one or more rectangles of at most
- * FK_RECT x FK_RECT pixels that share one filter, and appends them to one of FK_NCLASS lists
- * by tap count, so that each list can be rendered by a kernel launch whose shared-memory
- * layout fits its longest filter.  Inside a list, a frame's items are contiguous and ordered
- * by descending tap count.
+ * Work items.  The plan kernel turns the fragments of a frame into strips: rectangles at
+ * most FK_RECT pixels wide and FK_STRIP_ROWS pixels tall that share one filter -- vertically
+ * adjacent fragments with the same taps are merged, which is exact (every output pixel
+ * depends only on the image and its filter) and lets them share the horizontal pass over
+ * the 2r halo rows between them.  Strips are appended to one of FK_NCLASS lists by tap
+ * count, so that each list can be rendered by a kernel launch whose shared-memory layout
+ * fits its longest filter.  Inside a list, a frame's items are contiguous.
  */
 #define FK_RECT 32
+#define FK_STRIP_ROWS 128
 #define FK_NCLASS 4
 #define FK_CLASS_L0 31  /* class 0: L <= 31 (identity fragments included) */
 #define FK_CLASS_L1 55  /* class 1: L <= 55 */
@@ -59,15 +61,15 @@ struct fk_item {
 struct fk_plan_dev {
     int width, height, fragment;
     int cap;             /* per-frame stride of the cell arrays */
-    int nsub;            /* rectangles per fragment axis: ceil(fragment / FK_RECT) */
-    size_t items_cap;    /* entries per class list: max_frames * cap * nsub^2 */
+    int nsub_x;          /* strips per fragment across: ceil(fragment / FK_RECT) */
+    int nsub_y;          /* strips per fragment down: ceil(fragment / FK_STRIP_ROWS) */
+    size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */
     fk_item *items;      /* [FK_NCLASS][items_cap] */
     int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors */
     double *sigma;       /* [frames][cap] */
     int32_t *raw_length; /* [frames][cap] */
     int32_t *length;     /* [frames][cap], foveal cell forced to 1 */
     int32_t *offset;     /* [frames][cap], tap offset inside `taps` */
-    uint32_t *order;     /* [frames][cap], cell ids by descending tap count */
     int32_t *meta;       /* [frames][FK_META_WORDS] */
     const float *taps;   /* fp32 tap table the offsets index (canonical LUT or custom) */
 };

@@ -3,8 +3,8 @@
  *
  *   fk_plan_kernel   one CTA per frame: tiling shift, grid geometry, per-fragment
  *                    eccentricity -> sigma (fp64, bit-identical to the reference),
- *                    tap count, foveal-fragment forcing, and a cost-descending order of
- *                    the fragments for the render kernel.
+ *                    tap count, foveal-fragment forcing, and the render kernels' work
+ *                    items (same-filter strips, one list per tap-count class).
  *   fk_lut_kernel    Gaussian taps for every odd length (fp64 and fp32 copies).
  *
  * Reference arithmetic restated here (paths under /root/reference/pkg/src/foveakit/):
@@ -51,95 +51,84 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
     return idx > n - 1 ? n - 1 : idx;
 }
 
-/* Order the cells of frame f by descending tap count (counting sort on the radius) and
- * append them, as <= FK_RECT x FK_RECT rectangles, to the per-class work lists.
- * Called by all threads of the CTA that owns the frame; `length`, `offset` and the
- * frame's meta words must have been written by this CTA. */
-__device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *hist /*BINS*/,
-                              int *scan /*blockDim.x*/)
+/*
+ * Turn the cells of frame f into strips and append them to the per-class work lists.
+ * Called by all threads of the CTA that owns the frame; `length`, `offset` and the frame's
+ * meta words must have been written by this CTA.
+ *
+ * Fragments up to FK_RECT wide: vertically adjacent cells of one grid column with the same
+ * taps (length and offset) form runs; a run is cut into strips of at most
+ * FK_STRIP_ROWS / fragment cells.  Wider fragments are cut into columns FK_RECT wide (and
+ * pieces FK_STRIP_ROWS tall) without merging across cells.
+ */
+__device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
 {
     __shared__ int ccount[FK_NCLASS];
     __shared__ int cbase[FK_NCLASS];
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int i = tid; i < FK_SORT_BINS; i += nt) hist[i] = 0;
+    const int32_t *len = pd.length + (size_t)f * pd.cap;
+    const int32_t *off = pd.offset + (size_t)f * pd.cap;
+    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
+    const int sx = meta[FK_META_SX], sy = meta[FK_META_SY];
+    const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
+    const int F = pd.fragment;
+    const bool merge = F <= FK_RECT;
+    const int maxc = merge ? (FK_STRIP_ROWS / F > 1 ? FK_STRIP_ROWS / F : 1) : 1;
+    const int per_cell = merge ? 1 : pd.nsub_x * pd.nsub_y;
     if (tid < FK_NCLASS) ccount[tid] = 0;
     __syncthreads();
-    const int32_t *len = pd.length + (size_t)f * pd.cap;
-    for (int c = tid; c < ncells; c += nt) {
+
+    /* head of a strip and number of cells in it; 0 when the cell belongs to a strip above */
+    auto strip_cells = [&](int c) {
         const int L = len[c];
-        const int r = (L - 1) >> 1;
-        atomicAdd(&hist[r < FK_SORT_BINS ? r : FK_SORT_BINS - 1], 1);
-        atomicAdd(&ccount[fk_class_of(L)], 1);
-    }
+        if (!merge || L == 1) return 1;
+        const int gy = c / gw, gx = c - gy * gw;
+        const int o = off[c];
+        int above = 0;
+        for (int y = gy - 1; y >= 0 && len[y * gw + gx] == L && off[y * gw + gx] == o; y--) above++;
+        if (above % maxc != 0) return 0;
+        int n = 1;
+        while (n < maxc && gy + n < gh && len[(gy + n) * gw + gx] == L &&
+               off[(gy + n) * gw + gx] == o)
+            n++;
+        return n;
+    };
+
+    for (int c = tid; c < ncells; c += nt)
+        if (strip_cells(c) > 0) atomicAdd(&ccount[fk_class_of(len[c])], per_cell);
     __syncthreads();
-    /* suffix sums: base[b] = number of cells in bins > b.  Each thread owns a run of
-     * consecutive bins, highest first. */
-    const int per = (FK_SORT_BINS + nt - 1) / nt;
-    const int hi = FK_SORT_BINS - 1 - tid * per; /* first (highest) bin of this thread */
-    int local = 0;
-    for (int j = 0; j < per; j++) {
-        int b = hi - j;
-        if (b >= 0) local += hist[b];
-    }
-    scan[tid] = local;
-    __syncthreads();
-    const int nsub2 = pd.nsub * pd.nsub;
-    if (tid == 0) { /* nt <= 256 partial sums: serial exclusive scan is a few hundred ns */
-        int run = 0;
-        for (int i = 0; i < nt; i++) {
-            int v = scan[i];
-            scan[i] = run;
-            run += v;
-        }
-        /* one reservation per class keeps a frame's items contiguous in every list */
-        for (int k = 0; k < FK_NCLASS; k++)
-            cbase[k] = ccount[k] ? atomicAdd(&pd.counters[k], ccount[k] * nsub2) : 0;
-    }
-    __syncthreads();
-    int run = scan[tid];
-    for (int j = 0; j < per; j++) {
-        int b = hi - j;
-        if (b >= 0) {
-            int v = hist[b];
-            hist[b] = run;
-            run += v;
+    if (tid == 0) { /* one reservation per class keeps a frame's items contiguous */
+        for (int k = 0; k < FK_NCLASS; k++) {
+            cbase[k] = ccount[k] ? atomicAdd(&pd.counters[k], ccount[k]) : 0;
+            ccount[k] = 0; /* becomes the running slot inside the reservation */
         }
     }
     __syncthreads();
-    uint32_t *order = pd.order + (size_t)f * pd.cap;
     for (int c = tid; c < ncells; c += nt) {
-        int r = (len[c] - 1) >> 1;
-        int slot = atomicAdd(&hist[r < FK_SORT_BINS ? r : FK_SORT_BINS - 1], 1);
-        order[slot] = (uint32_t)c;
-    }
-    __syncthreads();
-    /* sorted slots [0, n3) are class 3, then class 2, 1, 0 (descending tap count) */
-    const int pre[FK_NCLASS] = {ccount[3] + ccount[2] + ccount[1], ccount[3] + ccount[2],
-                                ccount[3], 0};
-    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
-    const int sx = meta[FK_META_SX], sy = meta[FK_META_SY], gw = meta[FK_META_GW];
-    const int32_t *off = pd.offset + (size_t)f * pd.cap;
-    for (int c = tid; c < ncells; c += nt) {
-        const int cell = (int)order[c];
-        const int L = len[cell];
+        const int n = strip_cells(c);
+        if (n == 0) continue;
+        const int L = len[c];
         const int k = fk_class_of(L);
-        const int gy = cell / gw, gx = cell - gy * gw;
-        int x0, x1, y0, y1;
-        fk_span(pd.width, pd.fragment, sx, gx, x0, x1);
-        fk_span(pd.height, pd.fragment, sy, gy, y0, y1);
-        fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + (size_t)(c - pre[k]) * nsub2;
-        for (int s = 0; s < nsub2; s++) {
-            const int sby = s / pd.nsub, sbx = s - sby * pd.nsub;
-            const int rx0 = x0 + sbx * FK_RECT, ry0 = y0 + sby * FK_RECT;
+        const int gy = c / gw, gx = c - gy * gw;
+        int x0, x1, y0, y1, ye0, ye1;
+        fk_span(pd.width, F, sx, gx, x0, x1);
+        fk_span(pd.height, F, sy, gy, y0, y1);
+        fk_span(pd.height, F, sy, gy + n - 1, ye0, ye1);
+        (void)ye0;
+        y1 = ye1;
+        fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + atomicAdd(&ccount[k], per_cell);
+        for (int s = 0; s < per_cell; s++) {
+            const int sby = s / pd.nsub_x, sbx = s - sby * pd.nsub_x;
+            const int rx0 = x0 + sbx * FK_RECT, ry0 = y0 + sby * FK_STRIP_ROWS;
             int fw = x1 - rx0, fh = y1 - ry0;
             fw = fw < 0 ? 0 : (fw > FK_RECT ? FK_RECT : fw);
-            fh = fh < 0 ? 0 : (fh > FK_RECT ? FK_RECT : fh);
+            fh = fh < 0 ? 0 : (fh > FK_STRIP_ROWS ? FK_STRIP_ROWS : fh);
             if (fw == 0 || fh == 0) fw = fh = 0; /* empty: clipped edge fragment */
             fk_item it;
             it.frame = (uint32_t)f;
             it.xy = (uint32_t)rx0 | ((uint32_t)ry0 << 16);
             it.geom = (uint32_t)fw | ((uint32_t)L << 8) | ((uint32_t)fh << 21);
-            it.taps_off = (uint32_t)off[cell];
+            it.taps_off = (uint32_t)off[c];
             dst[s] = it;
         }
     }
@@ -148,8 +137,6 @@ __device__ void fk_sort_cells(const fk_plan_dev &pd, int f, int ncells, int *his
 __global__ void __launch_bounds__(FK_PLAN_THREADS)
 fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, int n_frames)
 {
-    __shared__ int hist[FK_SORT_BINS];
-    __shared__ int scan[FK_PLAN_THREADS];
     __shared__ int s_lmax;
     const int f = blockIdx.x;
     if (f >= n_frames) return;
@@ -222,16 +209,15 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
         meta[FK_META_LMAX] = s_lmax;
         meta[FK_META_STATUS] = 0;
     }
-    fk_sort_cells(pd, f, ncells, hist, scan);
+    __syncthreads();
+    fk_emit_items(pd, f, ncells);
 }
 
-/* Order pass for a caller-supplied grid (fk_plan_set_grid): frame 0 only. */
+/* Item emission for a caller-supplied grid (fk_plan_set_grid): frame 0 only. */
 __global__ void __launch_bounds__(FK_PLAN_THREADS) fk_order_kernel(fk_plan_dev pd)
 {
-    __shared__ int hist[FK_SORT_BINS];
-    __shared__ int scan[FK_PLAN_THREADS];
     const int32_t *meta = pd.meta;
-    fk_sort_cells(pd, 0, meta[FK_META_GW] * meta[FK_META_GH], hist, scan);
+    fk_emit_items(pd, 0, meta[FK_META_GW] * meta[FK_META_GH]);
 }
 
 /* filters.py:30-38 at sigma = L/6 (filters.py:78): one CTA per odd length. */
