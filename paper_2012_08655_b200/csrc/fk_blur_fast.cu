@@ -194,24 +194,37 @@ __device__ __forceinline__ void h_task(const float *__restrict__ trow,
  * Vertical task: acc[j][i] = sum_k g[k] * I[row0 + j + k][col0 + i], j < 8, i < 4.
  * `icol` points at I[row0][col0]; pitch in floats.  Same four-slot ring, over rows.
  */
+template <int NV>
 __device__ __forceinline__ void v_task(const float *__restrict__ ring, int pitch, int row0,
                                        int cap, const float *__restrict__ wts, int nchunk,
-                                       float (&acc)[kRV][4])
+                                       float (&acc)[kRV][NV])
 {
     /* `ring` points at column col0 of row 0 of the intermediate ring buffer of `cap` rows;
-     * row0 and cap are multiples of 4, so a group of four rows never straddles the wrap */
-    float4 win[16];
+     * row0 and cap are multiples of 4, so a group of four rows never straddles the wrap.
+     * NV = 4: one LDS.128 per row; NV = 3 (one RGB pixel): three conflict-free LDS.32. */
+    float win[16][NV];
+    auto load_row = [&](float (&dst)[NV], const float *src) {
+        if (NV == 4) {
+            const float4 x = *reinterpret_cast<const float4 *>(src);
+            dst[0] = x.x;
+            dst[1] = x.y;
+            dst[2] = x.z;
+            dst[NV - 1] = x.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < NV; i++) dst[i] = src[i];
+        }
+    };
 #pragma unroll
     for (int j = 0; j < kRV; j++)
 #pragma unroll
-        for (int i = 0; i < 4; i++) acc[j][i] = 0.0f;
+        for (int i = 0; i < NV; i++) acc[j][i] = 0.0f;
     int rp = row0;
 #pragma unroll
     for (int v = 0; v < 3; v++) {
         const float *base = ring + (size_t)rp * pitch;
 #pragma unroll
-        for (int t = 0; t < 4; t++)
-            win[4 * v + t] = *reinterpret_cast<const float4 *>(base + (size_t)t * pitch);
+        for (int t = 0; t < 4; t++) load_row(win[4 * v + t], base + (size_t)t * pitch);
         rp += 4;
         rp = rp >= cap ? rp - cap : rp;
     }
@@ -226,19 +239,16 @@ __device__ __forceinline__ void v_task(const float *__restrict__ ring, int pitch
             const float *nxt = ring + (size_t)rp * pitch;
 #pragma unroll
             for (int t = 0; t < 4; t++)
-                win[(4 * (p + 3) + t) % 16] =
-                    *reinterpret_cast<const float4 *>(nxt + (size_t)t * pitch);
+                load_row(win[(4 * (p + 3) + t) % 16], nxt + (size_t)t * pitch);
             rp += 4;
             rp = rp >= cap ? rp - cap : rp;
 #pragma unroll
             for (int t = 0; t < 4; t++) {
 #pragma unroll
                 for (int j = 0; j < kRV; j++) {
-                    const float4 x = win[(4 * p + t + j) % 16];
-                    acc[j][0] = fmaf(g[t], x.x, acc[j][0]);
-                    acc[j][1] = fmaf(g[t], x.y, acc[j][1]);
-                    acc[j][2] = fmaf(g[t], x.z, acc[j][2]);
-                    acc[j][3] = fmaf(g[t], x.w, acc[j][3]);
+#pragma unroll
+                    for (int i = 0; i < NV; i++)
+                        acc[j][i] = fmaf(g[t], win[(4 * p + t + j) % 16][i], acc[j][i]);
                 }
             }
         }
@@ -550,26 +560,37 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             }
             if (jend > jdone) { /* uniform across the CTA */
                 __syncthreads(); /* every warp's rows of this block are in the ring */
-                const int ntask = (jend - jdone) * ncg;
-                for (int task = tid; task < ntask; task += kThreads) {
-                    const int rg = jdone + task / ncg, cg = task % ncg;
-                    float acc[kRV][4];
-                    v_task(interm + cg * 4, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
-                    T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
-                    if (wide && rg * kRV + kRV <= fh) {
+                if (C == 3) {
+                    /* one task = one RGB pixel x 8 rows: 32 pixels x 4 groups fill the CTA */
+                    const int ntask = (jend - jdone) * fw;
+                    for (int task = tid; task < ntask; task += kThreads) {
+                        const int rg = jdone + task / fw, px = task % fw;
+                        float acc[kRV][3];
+                        v_task<3>(interm + px * 3, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
+                        T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0 + px) * 3;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
+                            if (rg * kRV + j < fh) {
 #pragma unroll
-                            for (int i = 0; i < 4; i++) orow[i] = fast_px<T>::store(acc[j][i]);
-                            orow += (size_t)W * C;
+                                for (int i = 0; i < 3; i++) orow[i] = fast_px<T>::store(acc[j][i]);
+                            }
+                            orow += (size_t)W * 3;
                         }
-                    } else {
+                    }
+                } else {
+                    const int ntask = (jend - jdone) * ncg;
+                    for (int task = tid; task < ntask; task += kThreads) {
+                        const int rg = jdone + task / ncg, cg = task % ncg;
+                        float acc[kRV][4];
+                        v_task<4>(interm + cg * 4, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
+                        T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
                             if (rg * kRV + j < fh) {
 #pragma unroll
                                 for (int i = 0; i < 4; i++)
-                                    if (cg * 4 + i < fw * C) orow[i] = fast_px<T>::store(acc[j][i]);
+                                    if (wide || cg * 4 + i < fw * C)
+                                        orow[i] = fast_px<T>::store(acc[j][i]);
                             }
                             orow += (size_t)W * C;
                         }
