@@ -28,11 +28,13 @@
  *               used as a four-slot ring with compile-time indices, one slot refilled by
  *               LDS.128 a whole chunk before it is read, so the inner loop is 32C FFMA
  *               per (C + 1) LDS.128 -- the FP32 pipe, not the LSU, is the limiter.
- *   V pass      one task = 8 output rows x 4 adjacent floats, same ring scheme over rows
- *               of the intermediate (128 FFMA per 5 LDS.128).  The intermediate itself is
- *               a ring of 2r + 40 rows in shared memory: after each 32-row block the
- *               output groups whose 8 + 2r rows are complete are rendered, so a strip of
- *               any height needs no more shared memory than a single fragment.
+ *   V pass      one task = 8 output rows x one RGB pixel (or 4 adjacent floats for gray),
+ *               same ring scheme over rows of the intermediate.  The intermediate itself
+ *               is a ring of 2r + 72 rows in shared memory: the output groups whose 8 + 2r
+ *               rows are complete after block b are rendered after the H pass of block
+ *               b + 1, ordered by two pairs of mbarriers instead of CTA barriers, so a
+ *               strip of any height needs no more shared memory than a single fragment
+ *               and warps only meet at a CTA barrier once per strip.
  *
  * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can
  * touch holds a finite value so 0 * garbage never produces a NaN.
@@ -90,6 +92,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
@@ -310,11 +316,13 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
     constexpr int IWP = NSEG_MAX * SEG + 4;               /* pitch/4 odd: 100 or 36 */
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw panels][mbarrier + counter, 16 B][colmap][2 x taps][tile][intermediate] */
+    /* layout: [raw panels][barriers, 64 B][colmap][2 x taps][tile][intermediate ring] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
     int *raw_done = reinterpret_cast<int *>(bar + 1);
-    int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 16);
+    uint64_t *hbar = bar + 2; /* [2] H pass of a block done by all warps (block parity) */
+    uint64_t *vbar = bar + 4; /* [2] V pass of a block done by all warps */
+    int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
     float *wts = reinterpret_cast<float *>(colmap + twp);
     float *tile = wts + 2 * wts_floats;
     float *interm = tile + kTB * twp;
@@ -352,6 +360,10 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     uint4 q_nxt = load_item(idx + stride);
     if (tid == 0) {
         if (TMA) mbar_init(bar, 1);
+        mbar_init(&hbar[0], kWarps);
+        mbar_init(&hbar[1], kWarps);
+        mbar_init(&vbar[0], kWarps);
+        mbar_init(&vbar[1], kWarps);
         *raw_done = 0;
     }
     /* the intermediate is a ring of icap rows; rows a padded tap can reach before they
@@ -364,6 +376,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 
     uint32_t phase = 0;
     int wsel = 0;
+    int nblocks = 0; /* 32-row blocks processed so far by this CTA (indexes hbar / vbar) */
     uint4 q_nn = none;
     for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wsel ^= 1) {
         q_nn = load_item(idx + 2 * stride); /* descriptor prefetch, two items ahead */
@@ -433,8 +446,58 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const int ngroups = (fh + kRV - 1) / kRV; /* groups of 8 output rows */
         const int ncg = (fw * C + 3) >> 2;        /* quads of output floats per row */
         const bool wide = (fw * C) % 4 == 0;
-        int jdone = 0, rbm = 0;                   /* groups rendered; rb mod icap */
-        for (int rb = 0; rb < th; rb += kTB) {
+        int jdone = 0, rbm = 0;                   /* groups released; rb mod icap */
+        int pend_b = 0, pend_e = 0;               /* groups released by the previous block */
+        /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over output groups
+         * [jb, je): 8 output rows each, read from the ring */
+        auto v_groups = [&](int jb, int je) {
+            if (C == 3) {
+                /* one task = one RGB pixel x 8 rows: 32 pixels x 4 groups fill the CTA */
+                const int ntask = (je - jb) * fw;
+                for (int task = tid; task < ntask; task += kThreads) {
+                    const int rg = jb + task / fw, px = task % fw;
+                    float acc[kRV][3];
+                    v_task<3>(interm + px * 3, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
+                    T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0 + px) * 3;
+#pragma unroll
+                    for (int j = 0; j < kRV; j++) {
+                        if (rg * kRV + j < fh) {
+#pragma unroll
+                            for (int i = 0; i < 3; i++) orow[i] = fast_px<T>::store(acc[j][i]);
+                        }
+                        orow += (size_t)W * 3;
+                    }
+                }
+            } else {
+                const int ntask = (je - jb) * ncg;
+                for (int task = tid; task < ntask; task += kThreads) {
+                    const int rg = jb + task / ncg, cg = task % ncg;
+                    float acc[kRV][4];
+                    v_task<4>(interm + cg * 4, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
+                    T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
+#pragma unroll
+                    for (int j = 0; j < kRV; j++) {
+                        if (rg * kRV + j < fh) {
+#pragma unroll
+                            for (int i = 0; i < 4; i++)
+                                if (wide || cg * 4 + i < fw * C)
+                                    orow[i] = fast_px<T>::store(acc[j][i]);
+                        }
+                        orow += (size_t)W * C;
+                    }
+                }
+            }
+        };
+        /*
+         * Software pipeline over 32-row blocks, no CTA-wide barrier inside an item:
+         *   block b:  convert own rows -> H into the ring -> arrive hbar(b)
+         *             -> wait hbar(b-1) -> V over the groups block b-1 released -> arrive vbar(b-1)
+         * The ring holds 2r + 72 rows, so H of block b only overwrites rows that V of
+         * block b-2 and older were reading (waited for through vbar), and a warp never
+         * waits for H work of the block it has just finished itself.
+         */
+        int b = 0;
+        for (int rb = 0; rb < th; rb += kTB, b++) {
             const int nrows = th - rb < kTB ? th - rb : kTB;
             const int ys = y0 - r + rb;
             const bool mine = warp * kWR < nrows; /* this warp owns rows of this block */
@@ -533,6 +596,8 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
                 __syncwarp();
             }
+            /* H of this block overwrites ring rows last read by V of block b-2 */
+            if (b >= 2) mbar_wait(&vbar[(nblocks + b - 2) & 1], ((nblocks + b - 2) >> 1) & 1);
             /* horizontal pass over this warp's rows (blockwise.py:151) into the ring */
             if (mine) {
                 for (int task = lane; task < kWR * nseg; task += 32) {
@@ -546,11 +611,11 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
             }
             __syncwarp(); /* the next block's conversion overwrites this warp's tile rows */
+            if (lane == 0) mbar_arrive(&hbar[(nblocks + b) & 1]);
             rbm += kTB;
             rbm = rbm >= icap ? rbm - icap : rbm;
 
-            /* ---- vertical pass (blockwise.py:152) + rounding (convolve.py:15) over the
-             * groups of 8 output rows whose 8 + 2r intermediate rows are all there ------ */
+            /* groups of 8 output rows whose 8 + 2r intermediate rows exist after this block */
             const int produced = rb + nrows;
             int jend = ngroups;
             if (produced < th) {
@@ -558,50 +623,23 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 jend = avail >= 0 ? avail / kRV + 1 : 0;
                 jend = jend < ngroups ? jend : ngroups;
             }
-            if (jend > jdone) { /* uniform across the CTA */
-                __syncthreads(); /* every warp's rows of this block are in the ring */
-                if (C == 3) {
-                    /* one task = one RGB pixel x 8 rows: 32 pixels x 4 groups fill the CTA */
-                    const int ntask = (jend - jdone) * fw;
-                    for (int task = tid; task < ntask; task += kThreads) {
-                        const int rg = jdone + task / fw, px = task % fw;
-                        float acc[kRV][3];
-                        v_task<3>(interm + px * 3, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
-                        T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0 + px) * 3;
-#pragma unroll
-                        for (int j = 0; j < kRV; j++) {
-                            if (rg * kRV + j < fh) {
-#pragma unroll
-                                for (int i = 0; i < 3; i++) orow[i] = fast_px<T>::store(acc[j][i]);
-                            }
-                            orow += (size_t)W * 3;
-                        }
-                    }
-                } else {
-                    const int ntask = (jend - jdone) * ncg;
-                    for (int task = tid; task < ntask; task += kThreads) {
-                        const int rg = jdone + task / ncg, cg = task % ncg;
-                        float acc[kRV][4];
-                        v_task<4>(interm + cg * 4, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
-                        T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
-#pragma unroll
-                        for (int j = 0; j < kRV; j++) {
-                            if (rg * kRV + j < fh) {
-#pragma unroll
-                                for (int i = 0; i < 4; i++)
-                                    if (wide || cg * 4 + i < fw * C)
-                                        orow[i] = fast_px<T>::store(acc[j][i]);
-                            }
-                            orow += (size_t)W * C;
-                        }
-                    }
-                }
-                jdone = jend;
-                /* the next block overwrites ring rows these groups were reading; after the
-                 * last block this also frees taps and column map for the next item */
-                __syncthreads();
+            if (b >= 1) { /* render what the PREVIOUS block released */
+                mbar_wait(&hbar[(nblocks + b - 1) & 1], ((nblocks + b - 1) >> 1) & 1);
+                v_groups(pend_b, pend_e);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&vbar[(nblocks + b - 1) & 1]);
             }
+            pend_b = jdone;
+            pend_e = jend;
+            jdone = jend;
         }
+        /* drain: the groups released by the last block */
+        mbar_wait(&hbar[(nblocks + b - 1) & 1], ((nblocks + b - 1) >> 1) & 1);
+        v_groups(pend_b, pend_e);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&vbar[(nblocks + b - 1) & 1]);
+        nblocks += b;
+        __syncthreads(); /* ring, taps and column map are free for the next item */
     }
 }
 
@@ -622,11 +660,11 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
     int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
-    /* ring of intermediate rows: 2r + 40 lets a block of 32 new rows be written while the
-     * rows the pending output groups still need stay intact (multiple of 4) */
-    l.irows = (2 * ((max_length - 1) / 2) + 40 + 3) & ~3;
+    /* ring of intermediate rows: 2r + 72 lets a block of 32 new rows be written while the
+     * previous block's output groups are still being rendered (multiple of 4) */
+    l.irows = (2 * ((max_length - 1) / 2) + 72 + 3) & ~3;
     l.npanel = tma ? (15 + twz + 4 + kPanelB - 1) / kPanelB : 0;
-    l.smem = (size_t)l.npanel * kPanelBytes + 16 + (size_t)twp * sizeof(int) +
+    l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)twp * sizeof(int) +
              ((size_t)2 * l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
     return l;
 }
