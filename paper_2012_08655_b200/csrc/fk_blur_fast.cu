@@ -496,8 +496,11 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
          * block b-2 and older were reading (waited for through vbar), and a warp never
          * waits for H work of the block it has just finished itself.
          */
-        int b = 0;
-        for (int rb = 0; rb < th; rb += kTB, b++) {
+        const int nblk = (th + kTB - 1) / kTB;
+        for (int b = 0; b <= nblk; b++) { /* iteration nblk only drains the last V groups */
+            const int rb = b * kTB;
+            int new_b = jdone, new_e = jdone;
+            if (b < nblk) {
             const int nrows = th - rb < kTB ? th - rb : kTB;
             const int ys = y0 - r + rb;
             const bool mine = warp * kWR < nrows; /* this warp owns rows of this block */
@@ -623,22 +626,19 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 jend = avail >= 0 ? avail / kRV + 1 : 0;
                 jend = jend < ngroups ? jend : ngroups;
             }
+            new_e = jend;
+            jdone = jend;
+            } /* b < nblk */
             if (b >= 1) { /* render what the PREVIOUS block released */
                 mbar_wait(&hbar[(nblocks + b - 1) & 1], ((nblocks + b - 1) >> 1) & 1);
                 v_groups(pend_b, pend_e);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&vbar[(nblocks + b - 1) & 1]);
             }
-            pend_b = jdone;
-            pend_e = jend;
-            jdone = jend;
+            pend_b = new_b;
+            pend_e = new_e;
         }
-        /* drain: the groups released by the last block */
-        mbar_wait(&hbar[(nblocks + b - 1) & 1], ((nblocks + b - 1) >> 1) & 1);
-        v_groups(pend_b, pend_e);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&vbar[(nblocks + b - 1) & 1]);
-        nblocks += b;
+        nblocks += nblk;
         __syncthreads(); /* ring, taps and column map are free for the next item */
     }
 }

@@ -36,7 +36,7 @@ enum {
 #define FK_RECT 32
 #define FK_STRIP_ROWS 128
 #define FK_NCLASS 4
-#define FK_CLASS_L0 31  /* class 0: L <= 31 (identity fragments included) */
+#define FK_CLASS_L0 27  /* class 0: L <= 27 (identity fragments included) */
 #define FK_CLASS_L1 55  /* class 1: L <= 55 */
 #define FK_CLASS_L2 127 /* class 2: L <= 127; class 3: longer (generic kernel) */
 
