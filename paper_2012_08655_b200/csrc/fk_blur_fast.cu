@@ -135,6 +135,40 @@ __device__ __forceinline__ float4 bytes_to_float4(uint32_t w)
 }
 
 /*
+ * Vector converter for one warp's kWR rows of a block whose rows need no clamping: tile
+ * word wj = raw bytes [skew + 4 wj, +4) = two aligned words and a funnel shift.  NP (the
+ * number of 32-word panels a row spans) is a template parameter so that the loads of four
+ * rows x NP words are issued back to back before the first conversion: independent
+ * chains, no branches; only the stores are predicated (lanes past the tile read other
+ * shared memory of this CTA, harmlessly).
+ */
+template <int NP>
+__device__ __forceinline__ void convert_rows_vec(const uint32_t *__restrict__ rp0,
+                                                 const uint32_t *__restrict__ rp1,
+                                                 float4 *__restrict__ tp, int tstride4, int bsh,
+                                                 const bool (&pred)[kMaxPanels - 1])
+{
+#pragma unroll 1
+    for (int i0 = 0; i0 < kWR; i0 += 4) {
+        uint32_t lo[4][NP], hi[4][NP];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                lo[i][p] = rp0[(i0 + i) * (kPanelB / 4) + p * kPanelWords];
+                hi[i][p] = rp1[(i0 + i) * (kPanelB / 4) + p * kPanelWords];
+            }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const float4 v = bytes_to_float4(__funnelshift_r(lo[i][p], hi[i][p], bsh));
+                if (pred[p]) tp[(i0 + i) * tstride4 + 32 * p] = v;
+            }
+    }
+}
+
+/*
  * Horizontal task: out[j] = sum_k g[k] * in[j + C*k], j in [0, 8C), for one tile row.
  * `trow` points at the first input float of the segment (16-byte aligned), `wts` at the
  * zero-padded taps, nchunk = ceil(L / 4).
@@ -347,13 +381,21 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         for (int p = 0; p < g.npanel; p++)
             tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
     };
-    /* zero-padded taps of an item into one of the two tap buffers (all threads) */
+    /* zero-padded taps of an item into one of the two tap buffers (all threads), with
+     * cp.async so nobody waits for the loads; src-size 0 writes the zero padding */
     auto fill_taps = [&](const uint4 q, float *dst) {
         const int L = (int)((q.z >> 8) & 0x1fffu);
         const int n = 4 * ((L + 3) >> 2) + 4;
         const float *taps = pd.taps + q.w;
-        for (int i = tid; i < n; i += kThreads) dst[i] = i < L ? taps[i] : 0.0f;
+        for (int i = tid; i < n; i += kThreads) {
+            const int in_range = i < L;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
+                         "l"(taps + (in_range ? i : 0)), "r"(in_range ? 4 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    auto taps_landed = [&]() { asm volatile("cp.async.wait_group 0;" ::: "memory"); };
 
     int idx = (int)blockIdx.x;
     uint4 q_cur = load_item(idx);
@@ -371,6 +413,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     for (int i = tid; i < icap * (IWP / 4); i += kThreads)
         reinterpret_cast<float4 *>(interm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (item_is_blur(q_cur)) fill_taps(q_cur, wts);
+    taps_landed();
     __syncthreads();
     if (TMA && tid == 0 && item_is_blur(q_cur)) issue(decode_item<C>(q_cur, W), 0);
 
@@ -400,6 +443,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             }
             /* all warps are aligned here and the raw buffer is idle */
             if (TMA && tid == 0 && next_blur) issue(decode_item<C>(q_nxt, W), 0);
+            taps_landed();
             __syncthreads();
             continue;
         }
@@ -529,19 +573,11 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         if (ys >= 0 && ys + kTB <= H) {
                             const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
                             const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
-#pragma unroll
-                            for (int i = 0; i < kWR; i++) {
-#pragma unroll
-                                for (int p = 0; p < kMaxPanels - 1; p++) {
-                                    if (p < np) { /* uniform */
-                                        const uint32_t lo = rp0[i * (kPanelB / 4) + p * kPanelWords];
-                                        const uint32_t hi = rp1[i * (kPanelB / 4) + p * kPanelWords];
-                                        const float4 v =
-                                            bytes_to_float4(__funnelshift_r(lo, hi, bsh));
-                                        if (pred[p]) tp[32 * p] = v;
-                                    }
-                                }
-                                tp += twp / 4;
+                            switch (np) {
+                            case 1: convert_rows_vec<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            case 2: convert_rows_vec<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            case 3: convert_rows_vec<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            default: convert_rows_vec<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
                             }
                         } else { /* rows clamp at the top / bottom edge of the image */
                             for (int i = 0; i < kWR; i++) {
@@ -639,6 +675,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             pend_e = new_e;
         }
         nblocks += nblk;
+        taps_landed();
         __syncthreads(); /* ring, taps and column map are free for the next item */
     }
 }
