@@ -296,14 +296,16 @@ def run_gpu(args):
     t_fp32 = flops / (fp32_nominal * 1e12)
     t_hbm = bytes_alg / (hbm_peak * 1e9)
     traffic = None
-    try:
-        traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(
-            "blur_dram_bytes_per_launch")
+    try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum of the render launches, per frame
+        per_frame = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(
+            "dram_bytes_per_frame")
+        traffic = per_frame * n if per_frame else None
     except Exception:
         pass
     roofline = {
         "bound": "fp32" if t_fp32 >= t_hbm else "hbm",
-        "kernel": "fk_blur (render of the whole batch, one launch per step)",
+        "kernel": ("fk_blur_fast (render of the whole batch: one persistent launch per "
+                   "tap-count class, up to 3 per step; timed together)"),
         "achieved": achieved_tf, "peak": fp32_nominal, "unit": "TFLOP/s",
         "frac": achieved_tf / fp32_nominal,
         "peak_source": (f"nominal FP32 = 2 x {eng.info['sm_count']} SMs x 128 lanes x "
