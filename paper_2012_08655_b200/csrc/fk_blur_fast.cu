@@ -326,7 +326,7 @@ template <int C> __device__ __forceinline__ item_geo decode_item(const uint4 q, 
     /* TMA needs the box to start on a 16-byte boundary of the row: fetch from the
      * aligned-down byte and skip `skew` bytes when converting */
     g.skew = g.xs_c * C - ((g.xs_c * C) & ~15);
-    g.npanel = (g.skew + g.twz + 4 + kPanelB - 1) / kPanelB;
+    g.npanel = (g.skew + g.tw + 4 + kPanelB - 1) / kPanelB; /* valid bytes only */
     return g;
 }
 
@@ -700,7 +700,7 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
     /* ring of intermediate rows: 2r + 72 lets a block of 32 new rows be written while the
      * previous block's output groups are still being rendered (multiple of 4) */
     l.irows = (2 * ((max_length - 1) / 2) + 72 + 3) & ~3;
-    l.npanel = tma ? (15 + twz + 4 + kPanelB - 1) / kPanelB : 0;
+    l.npanel = tma ? (15 + (kSub + 2 * ((max_length - 1) / 2)) * C + 4 + kPanelB - 1) / kPanelB : 0;
     l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)twp * sizeof(int) +
              ((size_t)2 * l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
     return l;

@@ -35,18 +35,26 @@ enum {
  */
 #define FK_RECT 32
 #define FK_STRIP_ROWS 128
-#define FK_NCLASS 4
-#define FK_CLASS_L0 27  /* class 0: L <= 27 (identity fragments included) */
-#define FK_CLASS_L1 55  /* class 1: L <= 55 */
-#define FK_CLASS_L2 127 /* class 2: L <= 127; class 3: longer (generic kernel) */
+#define FK_NCLASS 5
+/* Upper tap count of each class; the last class (longer filters) goes to the generic
+ * kernel.  The bounds are where the fast kernel's shared-memory layout loses a resident
+ * CTA per SM: 3 CTAs up to 27 taps, 2 up to 67, 1 up to 127. */
+#define FK_CLASS_L0 27
+#define FK_CLASS_L1 55
+#define FK_CLASS_L2 67
+#define FK_CLASS_L3 127
 
 static __host__ __device__ __forceinline__ int fk_class_of(int L)
 {
-    return L <= FK_CLASS_L0 ? 0 : (L <= FK_CLASS_L1 ? 1 : (L <= FK_CLASS_L2 ? 2 : 3));
+    return L <= FK_CLASS_L0 ? 0
+         : L <= FK_CLASS_L1 ? 1
+         : L <= FK_CLASS_L2 ? 2
+         : L <= FK_CLASS_L3 ? 3 : 4;
 }
 static inline int fk_class_lmax(int k)
 {
-    return k == 0 ? FK_CLASS_L0 : (k == 1 ? FK_CLASS_L1 : (k == 2 ? FK_CLASS_L2 : 8191));
+    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, FK_CLASS_L3, 8191};
+    return lmax[k];
 }
 
 /* 16 bytes, loaded as one uint4 by the render kernels. */
