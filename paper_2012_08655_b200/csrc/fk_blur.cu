@@ -130,6 +130,28 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
     }
 }
 
+/* blockwise.py:141-143: identity fragments (the copy list) are copied through. */
+template <typename T>
+__global__ void __launch_bounds__(256)
+fk_copy_items(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int C)
+{
+    const fk_item *items = pd.items + (size_t)FK_CLASS_COPY * pd.items_cap;
+    const int n_items = pd.counters[FK_CLASS_COPY];
+    const int W = pd.width, H = pd.height;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
+        const int fw = (int)(q.z & 0xffu), fh = (int)(q.z >> 21);
+        const int x0 = (int)(q.y & 0xffffu), y0 = (int)(q.y >> 16);
+        const size_t frame_off = (size_t)q.x * H * W * C;
+        const int rowlen = fw * C;
+        for (int i = threadIdx.x; i < fh * rowlen; i += blockDim.x) {
+            const int y = i / rowlen, c = i - y * rowlen;
+            const size_t o = frame_off + ((size_t)(y0 + y) * W + x0) * C + c;
+            out[o] = in[o];
+        }
+    }
+}
+
 /* FP32 peak probe: 16 independent FFMA chains per thread, no memory traffic. */
 __global__ void __launch_bounds__(256) fk_fp32_probe(float *out, int iters)
 {
@@ -196,12 +218,11 @@ cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, 
     /* rewind the render cursors (the counts stay) */
     cudaError_t e = cudaMemsetAsync(pd.counters + FK_NCLASS, 0, FK_NCLASS * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
-    for (int k = FK_NCLASS - 1; k >= 0; k--) {
-        const int lmin = k == 0 ? 1 : fk_class_lmax(k - 1) + 2;
-        if (lmin > bound_length) continue;
+    for (int k = FK_CLASS_GENERIC; k >= 0; k--) {
+        if (fk_class_lmin(k) > bound_length) continue;
         const int class_length = fk_class_lmax(k) < bound_length ? fk_class_lmax(k) : bound_length;
         bool taken = false;
-        if (h->variant != 1 && k < FK_NCLASS - 1) {
+        if (h->variant != 1 && k < FK_CLASS_GENERIC) {
             e = fk_launch_blur_fast(h, pd, k, in, out, n_frames, channels, is_f32, class_length,
                                     s, &taken);
             if (e != cudaSuccess) return e;
@@ -213,5 +234,12 @@ cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, 
         }
         *launches += 1;
     }
-    return cudaSuccess;
+    /* identity fragments */
+    const int grid = h->prop.multiProcessorCount * 4;
+    if (is_f32)
+        fk_copy_items<float><<<grid, 256, 0, s>>>(pd, (const float *)in, (float *)out, channels);
+    else
+        fk_copy_items<uint8_t><<<grid, 256, 0, s>>>(pd, (const uint8_t *)in, (uint8_t *)out, channels);
+    *launches += 1;
+    return cudaGetLastError();
 }

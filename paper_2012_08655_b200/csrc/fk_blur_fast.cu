@@ -330,11 +330,6 @@ template <int C> __device__ __forceinline__ item_geo decode_item(const uint4 q, 
     return g;
 }
 
-__device__ __forceinline__ bool item_is_blur(const uint4 q)
-{
-    return (q.z & 0xffu) != 0 && (q.z >> 21) != 0 && ((q.z >> 8) & 0x1fffu) > 1;
-}
-
 /*
  * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
  *              (W*C, H, N) with 128 x 32 x 1 boxes.
@@ -348,9 +343,9 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG_MAX = (kSub * C + SEG - 1) / SEG; /* 4 */
-    constexpr int IWP = NSEG_MAX * SEG + 4;               /* pitch/4 odd: 100 or 36 */
+    constexpr int IWP = NSEG_MAX * SEG;                   /* ring row pitch: 96 or 32 floats */
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw panels][barriers, 64 B][colmap][2 x taps][tile][intermediate ring] */
+    /* layout: [raw panels][barriers, 64 B][colmap][per-warp taps x 3][tile][ring] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
     int *raw_done = reinterpret_cast<int *>(bar + 1);
@@ -358,7 +353,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     uint64_t *vbar = bar + 4; /* [2] V pass of a block done by all warps */
     int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
     float *wts = reinterpret_cast<float *>(colmap + twp);
-    float *tile = wts + 2 * wts_floats;
+    float *tile = wts + kWarps * 3 * wts_floats;
     float *interm = tile + kTB * twp;
 
     const int W = pd.width, H = pd.height;
@@ -381,13 +376,15 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         for (int p = 0; p < g.npanel; p++)
             tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
     };
-    /* zero-padded taps of an item into one of the two tap buffers (all threads), with
-     * cp.async so nobody waits for the loads; src-size 0 writes the zero padding */
-    auto fill_taps = [&](const uint4 q, float *dst) {
+    /* Zero-padded taps of an item into one of THIS WARP's three tap buffers, with cp.async
+     * so nobody waits for the loads (src-size 0 writes the zero padding).  Per-warp copies
+     * mean no other warp has to be waited for before the taps are used. */
+    auto fill_taps = [&](const uint4 q, int slot) {
         const int L = (int)((q.z >> 8) & 0x1fffu);
         const int n = 4 * ((L + 3) >> 2) + 4;
         const float *taps = pd.taps + q.w;
-        for (int i = tid; i < n; i += kThreads) {
+        float *dst = wts + (warp * 3 + slot) * wts_floats;
+        for (int i = lane; i < n; i += 32) {
             const int in_range = i < L;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
                          "l"(taps + (in_range ? i : 0)), "r"(in_range ? 4 : 0)
@@ -395,7 +392,6 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto taps_landed = [&]() { asm volatile("cp.async.wait_group 0;" ::: "memory"); };
 
     int idx = (int)blockIdx.x;
     uint4 q_cur = load_item(idx);
@@ -412,41 +408,32 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
      * have been produced must hold finite values, so start from zeros */
     for (int i = tid; i < icap * (IWP / 4); i += kThreads)
         reinterpret_cast<float4 *>(interm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (item_is_blur(q_cur)) fill_taps(q_cur, wts);
-    taps_landed();
+    if (idx < n_items) fill_taps(q_cur, 0);
     __syncthreads();
-    if (TMA && tid == 0 && item_is_blur(q_cur)) issue(decode_item<C>(q_cur, W), 0);
+    if (TMA && tid == 0 && idx < n_items) issue(decode_item<C>(q_cur, W), 0);
 
     uint32_t phase = 0;
-    int wsel = 0;
+    int wslot = 0;   /* tap buffer of the current item (0..2) */
     int nblocks = 0; /* 32-row blocks processed so far by this CTA (indexes hbar / vbar) */
+    int rpos = 0;    /* ring row where the current item's first tile row goes (multiple of 4) */
     uint4 q_nn = none;
-    for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wsel ^= 1) {
+    /*
+     * The items of this CTA form one stream of 32-row blocks.  Inside and across items:
+     *   block B:  convert own rows -> wait vbar(B-2) -> H into the ring -> arrive hbar(B)
+     *             -> wait hbar(B-1) -> V over the groups block B-1 released -> arrive vbar(B-1)
+     * The ring holds 2r + 80 rows and continues across items, so H of block B only overwrites
+     * rows that V of block B-2 and older were reading, a warp never waits for work it has
+     * just finished itself, and there is no CTA-wide barrier on the vector path.
+     */
+    for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wslot = wslot == 2 ? 0 : wslot + 1) {
         q_nn = load_item(idx + 2 * stride); /* descriptor prefetch, two items ahead */
-        float *w_cur = wts + wsel * wts_floats;
-        float *w_nxt = wts + (wsel ^ 1) * wts_floats;
-        const bool next_blur = item_is_blur(q_nxt);
-        /* every item prepares its successor's taps; they become visible at the barrier
-         * that ends this item (the buffer was last read two items ago) */
-        if (next_blur) fill_taps(q_nxt, w_nxt);
-
-        if (!item_is_blur(q_cur)) {
-            const item_geo g = decode_item<C>(q_cur, W);
-            if (g.fw != 0 && g.fh != 0) { /* blockwise.py:141-143: identity fragments */
-                const size_t frame_off = (size_t)g.f * H * W * C;
-                const int rowlen = g.fw * C;
-                for (int i = tid; i < g.fh * rowlen; i += kThreads) {
-                    const int y = i / rowlen, c = i - y * rowlen;
-                    const size_t o = frame_off + ((size_t)(g.y0 + y) * W + g.x0) * C + c;
-                    out[o] = in[o];
-                }
-            }
-            /* all warps are aligned here and the raw buffer is idle */
-            if (TMA && tid == 0 && next_blur) issue(decode_item<C>(q_nxt, W), 0);
-            taps_landed();
-            __syncthreads();
-            continue;
-        }
+        const bool have_next = idx + stride < n_items;
+        const float *w_cur = wts + (warp * 3 + wslot) * wts_floats;
+        /* this item's taps were requested one item ago by this warp */
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        /* request the next item's; that buffer was last read by this warp two items ago */
+        if (have_next) fill_taps(q_nxt, wslot == 2 ? 0 : wslot + 1);
 
         const item_geo g = decode_item<C>(q_cur, W);
         const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
@@ -469,7 +456,10 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             __syncwarp();
         } else {
             /* clamp-to-edge by index.  TMA: tile column -> byte offset inside the box;
-             * plain loads: tile column -> element offset inside the image row */
+             * plain loads: tile column -> element offset inside the image row.  The map is
+             * shared by the CTA: one barrier so nobody still reads the previous one, one so
+             * everybody sees the new one. */
+            __syncthreads();
             for (int j = tid; j < twz; j += kThreads) {
                 int m = -1;
                 if (j < tw) {
@@ -490,26 +480,33 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const int ngroups = (fh + kRV - 1) / kRV; /* groups of 8 output rows */
         const int ncg = (fw * C + 3) >> 2;        /* quads of output floats per row */
         const bool wide = (fw * C) % 4 == 0;
-        int jdone = 0, rbm = 0;                   /* groups released; rb mod icap */
+        int jdone = 0, rbm = rpos;                /* groups released; ring row of block start */
         int pend_b = 0, pend_e = 0;               /* groups released by the previous block */
+        auto ring_row = [&](int k) { /* ring position of this item's tile row k (k < 2 icap) */
+            int p = rpos + k;
+            p = p >= icap ? p - icap : p;
+            return p >= icap ? p - icap : p;
+        };
         /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over output groups
          * [jb, je): 8 output rows each, read from the ring */
         auto v_groups = [&](int jb, int je) {
             if (C == 3) {
-                /* one task = one RGB pixel x 8 rows: 32 pixels x 4 groups fill the CTA */
-                const int ntask = (je - jb) * fw;
+                /* one task = one RGB pixel x 8 rows: a warp per group, a lane per pixel */
+                const int ntask = (je - jb) * 32;
                 for (int task = tid; task < ntask; task += kThreads) {
-                    const int rg = jb + task / fw, px = task % fw;
-                    float acc[kRV][3];
-                    v_task<3>(interm + px * 3, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
-                    T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0 + px) * 3;
+                    const int rg = jb + (task >> 5), px = task & 31;
+                    if (px < fw) {
+                        float acc[kRV][3];
+                        v_task<3>(interm + px * 3, IWP, ring_row(rg * kRV), icap, w_cur, nchunk, acc);
+                        T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0 + px) * 3;
 #pragma unroll
-                    for (int j = 0; j < kRV; j++) {
-                        if (rg * kRV + j < fh) {
+                        for (int j = 0; j < kRV; j++) {
+                            if (rg * kRV + j < fh) {
 #pragma unroll
-                            for (int i = 0; i < 3; i++) orow[i] = fast_px<T>::store(acc[j][i]);
+                                for (int i = 0; i < 3; i++) orow[i] = fast_px<T>::store(acc[j][i]);
+                            }
+                            orow += (size_t)W * 3;
                         }
-                        orow += (size_t)W * 3;
                     }
                 }
             } else {
@@ -517,7 +514,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 for (int task = tid; task < ntask; task += kThreads) {
                     const int rg = jb + task / ncg, cg = task % ncg;
                     float acc[kRV][4];
-                    v_task<4>(interm + cg * 4, IWP, (rg * kRV) % icap, icap, w_cur, nchunk, acc);
+                    v_task<4>(interm + cg * 4, IWP, ring_row(rg * kRV), icap, w_cur, nchunk, acc);
                     T *orow = dst + ((size_t)(y0 + rg * kRV) * W + x0) * C + cg * 4;
 #pragma unroll
                     for (int j = 0; j < kRV; j++) {
@@ -532,14 +529,6 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
             }
         };
-        /*
-         * Software pipeline over 32-row blocks, no CTA-wide barrier inside an item:
-         *   block b:  convert own rows -> H into the ring -> arrive hbar(b)
-         *             -> wait hbar(b-1) -> V over the groups block b-1 released -> arrive vbar(b-1)
-         * The ring holds 2r + 72 rows, so H of block b only overwrites rows that V of
-         * block b-2 and older were reading (waited for through vbar), and a warp never
-         * waits for H work of the block it has just finished itself.
-         */
         const int nblk = (th + kTB - 1) / kTB;
         for (int b = 0; b <= nblk; b++) { /* iteration nblk only drains the last V groups */
             const int rb = b * kTB;
@@ -554,11 +543,6 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 if (mine) {
                     const int ys_c = fast_clamp(ys, 0, H - 1);
                     if (vec) {
-                        /* tile word wj = raw bytes [skew + 4 wj, +4): two aligned words and
-                         * a funnel shift; lane-constant indices, row and panel steps are
-                         * immediates.  Loads are unconditional (a lane past the tile reads
-                         * other shared memory of this CTA, harmlessly), stores predicated:
-                         * branch-free, 8 x panels independent chains per lane. */
                         const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
                         const int bsh = (g.skew & 3) * 8;
                         const int w0 = lane + (g.skew >> 2), w1 = w0 + 1;
@@ -614,7 +598,7 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         *raw_done = 0;
                         if (rb + kTB < th)
                             issue(g, rb + kTB);
-                        else if (next_blur)
+                        else if (have_next)
                             issue(decode_item<C>(q_nxt, W), 0);
                     }
                 }
@@ -635,12 +619,14 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
                 __syncwarp();
             }
-            /* H of this block overwrites ring rows last read by V of block b-2 */
-            if (b >= 2) mbar_wait(&vbar[(nblocks + b - 2) & 1], ((nblocks + b - 2) >> 1) & 1);
+            /* H of this block overwrites ring rows last read by V of block B-2 */
+            if (nblocks + b >= 2)
+                mbar_wait(&vbar[(nblocks + b - 2) & 1], ((nblocks + b - 2) >> 1) & 1);
             /* horizontal pass over this warp's rows (blockwise.py:151) into the ring */
             if (mine) {
                 for (int task = lane; task < kWR * nseg; task += 32) {
-                    const int row = warp * kWR + task / nseg, seg = task % nseg;
+                    const int row = warp * kWR + (nseg == 4 ? task >> 2 : task / nseg);
+                    const int seg = nseg == 4 ? task & 3 : task % nseg;
                     if (row < nrows) {
                         int rr = rbm + row;
                         rr = rr >= icap ? rr - icap : rr;
@@ -675,8 +661,8 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             pend_e = new_e;
         }
         nblocks += nblk;
-        taps_landed();
-        __syncthreads(); /* ring, taps and column map are free for the next item */
+        rpos = (ring_row(th) + 3) & ~3; /* the next item continues the ring */
+        rpos = rpos >= icap ? rpos - icap : rpos;
     }
 }
 
@@ -689,7 +675,7 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
 {
     constexpr int SEG = 8 * C;
     constexpr int NSEG = (kSub * C + SEG - 1) / SEG;
-    constexpr int IWP = NSEG * SEG + 4;
+    constexpr int IWP = NSEG * SEG;
     fast_layout l;
     const int nchunk = (max_length + 3) / 4;
     l.wts_floats = 4 * nchunk + 4; /* one zero quad after the last chunk (tap prefetch) */
@@ -697,12 +683,14 @@ template <int C> fast_layout fast_layout_for(int max_length, bool tma)
     int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
-    /* ring of intermediate rows: 2r + 72 lets a block of 32 new rows be written while the
-     * previous block's output groups are still being rendered (multiple of 4) */
-    l.irows = (2 * ((max_length - 1) / 2) + 72 + 3) & ~3;
+    /* ring of intermediate rows: 2r + 80 lets a block of 32 new rows -- of this strip or of
+     * the next one -- be written while the previous block's output groups are still being
+     * rendered (multiple of 4) */
+    l.irows = (2 * ((max_length - 1) / 2) + 80 + 3) & ~3;
     l.npanel = tma ? (15 + (kSub + 2 * ((max_length - 1) / 2)) * C + 4 + kPanelB - 1) / kPanelB : 0;
     l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)twp * sizeof(int) +
-             ((size_t)2 * l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) * sizeof(float);
+             ((size_t)kWarps * 3 * l.wts_floats + (size_t)kTB * twp + (size_t)l.irows * IWP) *
+                 sizeof(float);
     return l;
 }
 

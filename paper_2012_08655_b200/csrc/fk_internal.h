@@ -36,25 +36,33 @@ enum {
 #define FK_RECT 32
 #define FK_STRIP_ROWS 128
 #define FK_NCLASS 5
-/* Upper tap count of each class; the last class (longer filters) goes to the generic
- * kernel.  The bounds are where the fast kernel's shared-memory layout loses a resident
- * CTA per SM: 3 CTAs up to 27 taps, 2 up to 67, 1 up to 127. */
-#define FK_CLASS_L0 27
-#define FK_CLASS_L1 55
-#define FK_CLASS_L2 67
-#define FK_CLASS_L3 127
+/* Classes 0..2 are rendered by the fast kernel, each launch with the shared-memory layout
+ * of the class's longest filter: 3 resident CTAs per SM up to 23 taps, 2 up to 63, 1 up to
+ * 127.  Class 3 (longer filters) goes to the generic kernel, class 4 holds the identity
+ * fragments (L = 1), which are plain copies. */
+#define FK_CLASS_L0 23
+#define FK_CLASS_L1 63
+#define FK_CLASS_L2 127
+#define FK_CLASS_GENERIC 3
+#define FK_CLASS_COPY 4
 
 static __host__ __device__ __forceinline__ int fk_class_of(int L)
 {
-    return L <= FK_CLASS_L0 ? 0
+    return L <= 1 ? FK_CLASS_COPY
+         : L <= FK_CLASS_L0 ? 0
          : L <= FK_CLASS_L1 ? 1
-         : L <= FK_CLASS_L2 ? 2
-         : L <= FK_CLASS_L3 ? 3 : 4;
+         : L <= FK_CLASS_L2 ? 2 : FK_CLASS_GENERIC;
 }
+/* longest / shortest filter a class can hold */
 static inline int fk_class_lmax(int k)
 {
-    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, FK_CLASS_L3, 8191};
+    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, 8191, 1};
     return lmax[k];
+}
+static inline int fk_class_lmin(int k)
+{
+    static const int lmin[FK_NCLASS] = {3, FK_CLASS_L0 + 2, FK_CLASS_L1 + 2, FK_CLASS_L2 + 2, 1};
+    return lmin[k];
 }
 
 /* 16 bytes, loaded as one uint4 by the render kernels. */

@@ -94,8 +94,33 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
         return n;
     };
 
-    for (int c = tid; c < ncells; c += nt)
-        if (strip_cells(c) > 0) atomicAdd(&ccount[fk_class_of(len[c])], per_cell);
+    /* rectangle s of the strip headed by cell c (n cells); false when it is empty, which
+     * happens for clipped fragments wider than FK_RECT */
+    auto sub_rect = [&](int c, int n, int s, int &rx0, int &ry0, int &fw, int &fh) {
+        const int gy = c / gw, gx = c - gy * gw;
+        int x0, x1, y0, y1, ye0, ye1;
+        fk_span(pd.width, F, sx, gx, x0, x1);
+        fk_span(pd.height, F, sy, gy, y0, y1);
+        fk_span(pd.height, F, sy, gy + n - 1, ye0, ye1);
+        (void)ye0;
+        y1 = ye1;
+        const int sby = s / pd.nsub_x, sbx = s - sby * pd.nsub_x;
+        rx0 = x0 + sbx * FK_RECT;
+        ry0 = y0 + sby * FK_STRIP_ROWS;
+        fw = x1 - rx0;
+        fh = y1 - ry0;
+        fw = fw > FK_RECT ? FK_RECT : fw;
+        fh = fh > FK_STRIP_ROWS ? FK_STRIP_ROWS : fh;
+        return fw > 0 && fh > 0;
+    };
+
+    for (int c = tid; c < ncells; c += nt) {
+        const int n = strip_cells(c);
+        if (n == 0) continue;
+        int cnt = 0, a, b2, w, h2;
+        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, s, a, b2, w, h2) ? 1 : 0;
+        if (cnt) atomicAdd(&ccount[fk_class_of(len[c])], cnt);
+    }
     __syncthreads();
     if (tid == 0) { /* one reservation per class keeps a frame's items contiguous */
         for (int k = 0; k < FK_NCLASS; k++) {
@@ -109,27 +134,18 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
         if (n == 0) continue;
         const int L = len[c];
         const int k = fk_class_of(L);
-        const int gy = c / gw, gx = c - gy * gw;
-        int x0, x1, y0, y1, ye0, ye1;
-        fk_span(pd.width, F, sx, gx, x0, x1);
-        fk_span(pd.height, F, sy, gy, y0, y1);
-        fk_span(pd.height, F, sy, gy + n - 1, ye0, ye1);
-        (void)ye0;
-        y1 = ye1;
-        fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + atomicAdd(&ccount[k], per_cell);
+        int cnt = 0, rx0, ry0, fw, fh;
+        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, s, rx0, ry0, fw, fh) ? 1 : 0;
+        if (cnt == 0) continue;
+        fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + atomicAdd(&ccount[k], cnt);
         for (int s = 0; s < per_cell; s++) {
-            const int sby = s / pd.nsub_x, sbx = s - sby * pd.nsub_x;
-            const int rx0 = x0 + sbx * FK_RECT, ry0 = y0 + sby * FK_STRIP_ROWS;
-            int fw = x1 - rx0, fh = y1 - ry0;
-            fw = fw < 0 ? 0 : (fw > FK_RECT ? FK_RECT : fw);
-            fh = fh < 0 ? 0 : (fh > FK_STRIP_ROWS ? FK_STRIP_ROWS : fh);
-            if (fw == 0 || fh == 0) fw = fh = 0; /* empty: clipped edge fragment */
+            if (!sub_rect(c, n, s, rx0, ry0, fw, fh)) continue;
             fk_item it;
             it.frame = (uint32_t)f;
             it.xy = (uint32_t)rx0 | ((uint32_t)ry0 << 16);
             it.geom = (uint32_t)fw | ((uint32_t)L << 8) | ((uint32_t)fh << 21);
             it.taps_off = (uint32_t)off[c];
-            dst[s] = it;
+            *dst++ = it;
         }
     }
 }
