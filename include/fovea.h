@@ -123,6 +123,15 @@ int fk_plan_cell_capacity(const fk_plan *p); /* per-frame stride of the cell arr
 int fk_plan_model(fk_plan *p, const fk_params *params, int n_frames, const double *fix_xy,
                   int fix_on_device, void *stream);
 
+/* Replaces ingest_density_map (retinal.py:180-231) and the density branch of plan
+ * (blockwise.py:208-213): the 1-channel map (host memory, map_h x map_w bytes) is resampled
+ * bilinearly at the fragment midpoints of every frame's shifted tiling and
+ * sigma = sigma_max * (1 - v / 255); tap counts, foveal forcing and work items follow as in
+ * fk_plan_model.  Of `params` only fragment_size, use_shift and shift_x/y are used. */
+int fk_plan_density(fk_plan *p, const fk_params *params, int n_frames, const double *fix_xy,
+                    int fix_on_device, const uint8_t *map_host, int map_w, int map_h,
+                    double sigma_max, void *stream);
+
 /* Replaces render()'s use of an arbitrary (BlurGrid, FilterBank) pair
  * (blockwise.py:156-186) for ONE frame: the caller supplies the shift, the per-cell tap
  * counts (odd, >= 1) and offsets into `coeffs` (FilterBank.cumulative_sizes layout,

@@ -285,6 +285,7 @@ int fk_plan_destroy(fk_plan *p)
     cudaFree(p->d.meta);
     cudaFree(p->fix_dev);
     cudaFree(p->custom_taps);
+    cudaFree(p->density_map);
     delete p;
     return FK_OK;
 }
@@ -345,7 +346,72 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     p->d.taps = h->lut32;
     p->custom = 0;
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
-    FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, s));
+    const fk_density_dev no_density = {nullptr, 0, 0, 0.0};
+    FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, no_density, s));
+    h->launches++;
+    p->n_frames = n_frames;
+    p->bound_length = bound;
+    return FK_OK;
+}
+
+int fk_plan_density(fk_plan *p, const fk_params *prm, int n_frames, const double *fix_xy,
+                    int fix_on_device, const uint8_t *map_host, int map_w, int map_h,
+                    double sigma_max, void *stream)
+{
+    if (!p || !prm || !fix_xy || !map_host)
+        return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");
+    fk_handle *h = p->h;
+    if (n_frames < 1 || n_frames > p->max_frames)
+        return fk_fail(h, FK_EINVAL, "n_frames %d outside [1, %d]", n_frames, p->max_frames);
+    if (prm->fragment_size != p->d.fragment)
+        return fk_fail(h, FK_EINVAL, "params.fragment_size %d differs from the plan's %d",
+                       prm->fragment_size, p->d.fragment);
+    if (prm->use_shift == 2 && (prm->shift_x < 0 || prm->shift_x >= prm->fragment_size ||
+                                prm->shift_y < 0 || prm->shift_y >= prm->fragment_size))
+        return fk_fail(h, FK_EINVAL, "offset (%d, %d) outside [0, %d)", prm->shift_x,
+                       prm->shift_y, prm->fragment_size);
+    if (map_w < 1 || map_h < 1)
+        return fk_fail(h, FK_EINVAL, "image dimensions must be positive, got %dx%d", map_w, map_h);
+    if (!(sigma_max >= 0) || !std::isfinite(sigma_max)) /* retinal.py:221-222 */
+        return fk_fail(h, FK_EINVAL, "sigma_max must be >= 0, got %g", sigma_max);
+    const int W = p->d.width, H = p->d.height;
+    if (!fix_on_device)
+        for (int i = 0; i < n_frames; i++) {
+            double fx = fix_xy[2 * i], fy = fix_xy[2 * i + 1];
+            if (!(fx >= 0 && fx < W && fy >= 0 && fy < H))
+                return fk_fail(h, FK_EINVAL, "fixation (%g, %g) outside %dx%d image", fx, fy, W, H);
+        }
+    int bound = fk_length_of_sigma(sigma_max); /* sigma = sigma_max * (1 - v/255) <= sigma_max */
+    if (bound < 0 || bound + 2 > 8191)
+        return fk_fail(h, FK_EINVAL, "sigma values must be finite and >= 0 and need <= 8191 taps");
+    bound += 2;
+    FK_CUDA(h, cudaSetDevice(h->device));
+    if (bound > h->lut_max) {
+        int rc = fk_build_lut(h, bound, stream);
+        if (rc != FK_OK) return rc;
+    }
+    cudaStream_t s = as_stream(stream);
+    const size_t map_bytes = (size_t)map_w * map_h;
+    if (map_bytes > p->density_cap) {
+        FK_CUDA(h, cudaStreamSynchronize(s));
+        cudaFree(p->density_map);
+        p->density_map = nullptr;
+        p->density_cap = 0;
+        FK_CUDA(h, cudaMalloc(&p->density_map, map_bytes));
+        p->density_cap = map_bytes;
+    }
+    FK_CUDA(h, cudaMemcpyAsync(p->density_map, map_host, map_bytes, cudaMemcpyHostToDevice, s));
+    const double *fix_dev = fix_xy;
+    if (!fix_on_device) {
+        FK_CUDA(h, cudaMemcpyAsync(p->fix_dev, fix_xy, (size_t)n_frames * 2 * sizeof(double),
+                                   cudaMemcpyHostToDevice, s));
+        fix_dev = p->fix_dev;
+    }
+    p->d.taps = h->lut32;
+    p->custom = 0;
+    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
+    const fk_density_dev den = {p->density_map, map_w, map_h, sigma_max};
+    FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, den, s));
     h->launches++;
     p->n_frames = n_frames;
     p->bound_length = bound;

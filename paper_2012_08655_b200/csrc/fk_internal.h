@@ -90,6 +90,13 @@ struct fk_plan_dev {
     const float *taps;   /* fp32 tap table the offsets index (canonical LUT or custom) */
 };
 
+/* Density-map source of the sigma field (map == nullptr: retinal model). */
+struct fk_density_dev {
+    const uint8_t *map; /* device, map_h x map_w */
+    int map_w, map_h;
+    double sigma_max;
+};
+
 struct fk_handle {
     int device = -1;
     cudaDeviceProp prop{};
@@ -122,6 +129,8 @@ struct fk_plan {
     float *custom_taps = nullptr;
     int custom_cap = 0;
     double *fix_dev = nullptr; /* [max_frames][2] staging for host fixations */
+    uint8_t *density_map = nullptr; /* device copy of the last density map */
+    size_t density_cap = 0;
     fk_plan_dev d{};
 };
 
@@ -137,7 +146,7 @@ int fk_cuda_fail(fk_handle *h, cudaError_t e, const char *what);
 /* kernels (fk_plan.cu, fk_blur.cu) */
 cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cudaStream_t s);
 cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
-                           const double *fix_dev, cudaStream_t s);
+                           const double *fix_dev, const fk_density_dev &den, cudaStream_t s);
 cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s);
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,

@@ -151,7 +151,8 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
 }
 
 __global__ void __launch_bounds__(FK_PLAN_THREADS)
-fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, int n_frames)
+fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, int n_frames,
+               fk_density_dev den)
 {
     __shared__ int s_lmax;
     const int f = blockIdx.x;
@@ -194,12 +195,34 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
         fk_span(H, F, sy, gy, y0, y1);
         const double mx = __ddiv_rn((double)(x0 + x1), 2.0);          /* tiling.py:33 */
         const double my = __ddiv_rn((double)(y0 + y1), 2.0);
-        const double d = fk_hypot(__dsub_rn(mx, fx), __dsub_rn(my, fy)); /* retinal.py:110 */
-        const double e = __dmul_rn(__ddiv_rn(d, prm.d_corner), prm.e_corner); /* :112 */
-        const double fdeg = __dmul_rn(                                  /* retinal.py:129 */
-            __ddiv_rn(prm.e2, __dmul_rn(prm.alpha, __dadd_rn(e, prm.e2))), prm.log_inv_ct0);
-        const double fpix = __ddiv_rn(__dmul_rn(0.5, fdeg), prm.fmax);  /* retinal.py:140 */
-        const double s = __ddiv_rn(prm.strength, __dmul_rn(prm.two_pi, fpix)); /* :155 */
+        double s;
+        if (den.map != nullptr) {
+            /* retinal.py:180-231: _map_coords, _bilinear, _density_to_sigma */
+            const double mw = (double)den.map_w, mh = (double)den.map_h;
+            double u = __dsub_rn(__dmul_rn(__dadd_rn(mx, 0.5), __ddiv_rn(mw, (double)W)), 0.5);
+            double v = __dsub_rn(__dmul_rn(__dadd_rn(my, 0.5), __ddiv_rn(mh, (double)H)), 0.5);
+            u = fmin(fmax(u, 0.0), __dsub_rn(mw, 1.0));
+            v = fmin(fmax(v, 0.0), __dsub_rn(mh, 1.0));
+            const int u0 = (int)floor(u), v0 = (int)floor(v);
+            const int u1 = u0 + 1 < den.map_w - 1 ? u0 + 1 : den.map_w - 1;
+            const int v1 = v0 + 1 < den.map_h - 1 ? v0 + 1 : den.map_h - 1;
+            const double fu = __dsub_rn(u, (double)u0), fv = __dsub_rn(v, (double)v0);
+            const double m00 = (double)den.map[(size_t)v0 * den.map_w + u0];
+            const double m01 = (double)den.map[(size_t)v0 * den.map_w + u1];
+            const double m10 = (double)den.map[(size_t)v1 * den.map_w + u0];
+            const double m11 = (double)den.map[(size_t)v1 * den.map_w + u1];
+            const double top = __dadd_rn(__dmul_rn(m00, __dsub_rn(1.0, fu)), __dmul_rn(m01, fu));
+            const double bot = __dadd_rn(__dmul_rn(m10, __dsub_rn(1.0, fu)), __dmul_rn(m11, fu));
+            const double smp = __dadd_rn(__dmul_rn(top, __dsub_rn(1.0, fv)), __dmul_rn(bot, fv));
+            s = __dmul_rn(den.sigma_max, __dsub_rn(1.0, __ddiv_rn(smp, 255.0)));
+        } else {
+            const double d = fk_hypot(__dsub_rn(mx, fx), __dsub_rn(my, fy)); /* retinal.py:110 */
+            const double e = __dmul_rn(__ddiv_rn(d, prm.d_corner), prm.e_corner); /* :112 */
+            const double fdeg = __dmul_rn(                                  /* retinal.py:129 */
+                __ddiv_rn(prm.e2, __dmul_rn(prm.alpha, __dadd_rn(e, prm.e2))), prm.log_inv_ct0);
+            const double fpix = __ddiv_rn(__dmul_rn(0.5, fdeg), prm.fmax);  /* retinal.py:140 */
+            s = __ddiv_rn(prm.strength, __dmul_rn(prm.two_pi, fpix));       /* retinal.py:155 */
+        }
         sigma[c] = s;
         /* filters.py:25-26.  Non-finite or huge sigma saturates; the host rejects such
          * parameter sets before launching (SigmaField validation, retinal.py:93-94). */
@@ -282,9 +305,9 @@ cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cud
 }
 
 cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
-                           const double *fix_dev, cudaStream_t s)
+                           const double *fix_dev, const fk_density_dev &den, cudaStream_t s)
 {
-    fk_plan_kernel<<<n_frames, FK_PLAN_THREADS, 0, s>>>(pd, prm, fix_dev, n_frames);
+    fk_plan_kernel<<<n_frames, FK_PLAN_THREADS, 0, s>>>(pd, prm, fix_dev, n_frames, den);
     return cudaGetLastError();
 }
 

@@ -84,6 +84,24 @@ class DevicePlan:
         self.n_frames = n
         return self
 
+    def density(self, density_map, sigma_max, fragment_size, fixations, use_shift=True,
+                shift=None, stream=None):
+        """Plan from a 1-channel density map shared by all frames (fk_plan_density)."""
+        eng = self.engine
+        dm = np.ascontiguousarray(density_map, dtype=np.uint8)
+        if dm.ndim != 2:
+            raise ValueError("density map must be a 2-D uint8 array")
+        mode, sx, sy = (1 if use_shift else 0), 0, 0
+        if shift is not None:
+            mode, (sx, sy) = 2, (int(shift[0]), int(shift[1]))
+        prm = FkParams(fragment_size=int(fragment_size), use_shift=mode, shift_x=sx, shift_y=sy)
+        fix = np.ascontiguousarray(np.asarray(fixations, dtype=np.float64).reshape(-1, 2))
+        check(eng._lib.fk_plan_density(self._p, C.byref(prm), fix.shape[0], _np_ptr(fix), 0,
+                                       _np_ptr(dm), dm.shape[1], dm.shape[0],
+                                       C.c_double(float(sigma_max)), eng._stream(stream)), eng._h)
+        self.n_frames = fix.shape[0]
+        return self
+
     def set_grid(self, shift, lengths, offsets, coeffs, stream=None):
         """Install a caller-supplied (grid, bank) pair for one frame (fk_plan_set_grid)."""
         eng = self.engine

@@ -65,3 +65,21 @@ def frame_f32(seed, shape):
     return np.random.default_rng(seed).random(shape, dtype=np.float32)
 
 
+
+
+# name, map seed, (mh, mw), (W, H), F, shift, sigma_max  -- density-map sigma fields
+DENSITY_CASES = [
+    ("d_8x8_64_f16", 31, (8, 8), (64, 64), 16, (0, 0), 6.0),
+    ("d_23x37_301x203_f12", 32, (23, 37), (301, 203), 12, (5, 11), 4.5),
+    ("d_64x48_640x360_f32", 33, (64, 48), (640, 360), 32, (17, 3), 9.0),
+    ("d_3x5_1920x1080_f32", 34, (3, 5), (1920, 1080), 32, (16, 12), 12.0),
+]
+
+# name, image seed, (H, W, C), map seed, (mh, mw), params kwargs, sigma_max -- rendered output
+DENSITY_RENDER_CASES = [
+    ("dr_rgb_120x160_f16", 41, (120, 160, 3), 42, (9, 13), dict(fragment_size=16, fixation=(70, 50)), 5.0),
+]
+
+
+def density_map(seed, shape):
+    return np.random.default_rng(seed).integers(0, 256, shape, dtype=np.uint8)

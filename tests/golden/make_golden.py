@@ -31,8 +31,8 @@ from foveakit.imaging import RasterImage  # noqa: E402
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE))
 
-from cases import (BIG_RENDER_CASES, F32_CASES, PLAN_CASES, RENDER_CASES,  # noqa: E402
-                   frame_f32, frame_u8)
+from cases import (BIG_RENDER_CASES, DENSITY_CASES, DENSITY_RENDER_CASES, F32_CASES,  # noqa: E402
+                   PLAN_CASES, RENDER_CASES, density_map, frame_f32, frame_u8)
 
 
 def ref_plan(size, kw, use_shift):
@@ -125,6 +125,20 @@ def main():
                                   fragment_size=32, foveal_cell=(0, 0))
         uni[f"L{length}/out"] = blockwise.render(RasterImage.from_array(img), grid, bank).data
     np.savez_compressed(HERE / "renders_uniform.npz", **uni)
+
+    den = {}
+    for name, seed, mshape, size, F, shift, smax in DENSITY_CASES:
+        dm = RasterImage.from_array(density_map(seed, mshape))
+        den[f"{name}/sigma"] = retinal.ingest_density_map(dm, smax, size, F, shift).sigma
+    for name, seed, shape, mseed, mshape, kw, smax in DENSITY_RENDER_CASES:
+        img = frame_u8(seed, shape)
+        dm = RasterImage.from_array(density_map(mseed, mshape))
+        out, grid, bank, stats = blockwise.foveate(
+            RasterImage.from_array(img), retinal.FoveationParams(**kw), density=dm, sigma_max=smax)
+        den[f"{name}/out"] = out.data
+        den[f"{name}/index"] = grid.index
+        den[f"{name}/bank_lengths"] = bank.lengths
+    np.savez_compressed(HERE / "density.npz", **den)
 
     print("foveakit", foveakit.__name__, "numpy", np.__version__)
     for f in sorted(HERE.glob("*.npz")):
