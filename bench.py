@@ -29,20 +29,21 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-W, H, C, F = 1920, 1080, 3, 32
+W, H, C, F = 1920, 1080, 3, 32   # BASELINE configs[1]; --width/--height/--fragment explore others
 BATCH = 256
 METRIC = "foveated frames/sec at 1920x1080 RGB"
 WORKLOAD = ("batch of 256 synthetic 1920x1080 RGB uint8 frames, per-frame moving fixation, "
             "32x32 fragments (BASELINE configs[1])")
 
 
-def moving_fixations(n):
-    """fx = floor(960 + 768 cos(2 pi i / n)), fy = floor(540 + 432 sin)."""
+def moving_fixations(n, w=1920, h=1080):
+    """fx = floor(960 + 768 cos(2 pi i / n)), fy = floor(540 + 432 sin)
+    (scaled with the frame size for the exploration workloads)."""
     import numpy as np
 
     i = np.arange(n, dtype=np.float64)
-    fx = np.floor(960 + 768 * np.cos(2 * np.pi * i / n))
-    fy = np.floor(540 + 432 * np.sin(2 * np.pi * i / n))
+    fx = np.floor(w / 2 + 0.4 * w * np.cos(2 * np.pi * i / n))
+    fy = np.floor(h / 2 + 0.4 * h * np.sin(2 * np.pi * i / n))
     return np.ascontiguousarray(np.stack([fx, fy], axis=1))
 
 
@@ -234,13 +235,19 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    global W, H, F
+    W, H, F = args.width, args.height, args.fragment
+    explore = (W, H, F, args.dtype, args.e2) != (1920, 1080, 32, "u8", 2.3)
     eng = fk.get_engine(local)
-    params = fk.FoveationParams(fragment_size=F)
+    params = fk.FoveationParams(fragment_size=F, e2=args.e2)
     n = args.frames
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    frames = torch.randint(0, 256, (n, H, W, C), dtype=torch.uint8, device="cuda", generator=gen)
+    if args.dtype == "u8":
+        frames = torch.randint(0, 256, (n, H, W, C), dtype=torch.uint8, device="cuda", generator=gen)
+    else:
+        frames = torch.rand((n, H, W, C), dtype=torch.float32, device="cuda", generator=gen)
     out = torch.empty_like(frames)
-    fixes = moving_fixations(n)
+    fixes = moving_fixations(n, W, H)
     if args.fixation == "centre":       # exploration only; the reported workload is "moving"
         fixes[:] = (W / 2.0, H / 2.0)
     elif args.fixation == "corner":
@@ -280,7 +287,7 @@ def run_gpu(args):
     # roofline of the blur kernel: algorithmic FLOPs of this batch's plans / its duration
     lengths, meta = plan.read_lengths()
     flops = costs.batch_flops((W, H), F, C, lengths, meta)
-    bytes_alg = n * costs.frame_bytes((W, H), C, 1)
+    bytes_alg = n * costs.frame_bytes((W, H), C, frames.element_size())
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -322,8 +329,10 @@ def run_gpu(args):
 
     # end to end: pinned host frames -> public API -> pinned host frames
     e2e_n = args.e2e_frames
-    h_in = fk.pinned_empty((e2e_n, H, W, C), np.uint8)
-    h_out = fk.pinned_empty((e2e_n, H, W, C), np.uint8)
+    e2e_n = min(e2e_n, n)
+    np_dtype = np.uint8 if args.dtype == "u8" else np.float32
+    h_in = fk.pinned_empty((e2e_n, H, W, C), np_dtype)
+    h_out = fk.pinned_empty((e2e_n, H, W, C), np_dtype)
     h_in[...] = frames[:e2e_n].cpu().numpy()
     fix_host = fixes[:e2e_n]
     for _ in range(max(1, min(args.warmup, 3))):
@@ -344,7 +353,7 @@ def run_gpu(args):
            "matches_device_path": same}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not explore:
         del h_in, h_out
         cpu = cpu_baseline_leg(fixes)
 
@@ -354,7 +363,10 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "frames_per_gpu": n, "fragment_size": F,
+            "config": {"workload": WORKLOAD if not explore else
+                       f"exploration: {n} x {W}x{H} RGB {args.dtype} frames, moving fixation, "
+                       f"{F}x{F} fragments, e2={args.e2}",
+                       "frames_per_gpu": n, "fragment_size": F,
                        "l2_policy": "inputs larger than L2 (1.59 GB in + 1.59 GB out per step)",
                        "step": "fk_plan_model + fk_render_u8 over the whole batch"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
@@ -378,6 +390,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fixation", default="moving", choices=["moving", "centre", "corner"],
                     help="exploration only; BASELINE configs[1] is 'moving'")
+    ap.add_argument("--width", type=int, default=1920, help="exploration only")
+    ap.add_argument("--height", type=int, default=1080, help="exploration only")
+    ap.add_argument("--fragment", type=int, default=32, help="exploration only")
+    ap.add_argument("--dtype", default="u8", choices=["u8", "f32"], help="exploration only")
+    ap.add_argument("--e2", type=float, default=2.3, help="exploration only (CSF fit)")
     ap.add_argument("--fix-host", action="store_true",
                     help="exploration only: pass fixations from host memory each step")
     args = ap.parse_args()

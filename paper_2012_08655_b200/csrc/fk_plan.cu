@@ -56,10 +56,15 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  * Called by all threads of the CTA that owns the frame; `length`, `offset` and the frame's
  * meta words must have been written by this CTA.
  *
- * Fragments up to FK_RECT wide: vertically adjacent cells of one grid column with the same
- * taps (length and offset) form runs; a run is cut into strips of at most
- * FK_STRIP_ROWS / fragment cells.  Wider fragments are cut into columns FK_RECT wide (and
- * pieces FK_STRIP_ROWS tall) without merging across cells.
+ * Fragments up to FK_RECT wide are merged in two steps, both exact (an output pixel depends
+ * only on the image and its filter):
+ *   across  m = FK_RECT / F neighbouring cells of a grid row (aligned groups after the
+ *           leading partial cell) become one unit FK_RECT wide when they share their taps;
+ *   down    vertically adjacent equal units (same cells, same taps) inside an aligned block
+ *           of FK_STRIP_ROWS / F grid rows become one strip, which lets them share the
+ *           horizontal pass over the 2r halo rows between them.
+ * Wider fragments are cut into columns FK_RECT wide (and pieces FK_STRIP_ROWS tall) without
+ * merging across cells.
  */
 __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
 {
@@ -74,36 +79,60 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     const int F = pd.fragment;
     const bool merge = F <= FK_RECT;
     const int maxc = merge ? (FK_STRIP_ROWS / F > 1 ? FK_STRIP_ROWS / F : 1) : 1;
+    const int mgrp = merge ? FK_RECT / F : 1; /* cells per horizontal unit */
+    const int lead = sx > 0 ? 1 : 0;
     const int per_cell = merge ? 1 : pd.nsub_x * pd.nsub_y;
     if (tid < FK_NCLASS) ccount[tid] = 0;
     __syncthreads();
 
-    /* head of a strip and number of cells in it; 0 when the cell belongs to a strip above */
-    auto strip_cells = [&](int c) {
-        const int L = len[c];
-        if (!merge || L == 1) return 1;
+    /* the unit [u0, u1) of grid row gy that contains cell gx */
+    auto unit_of = [&](int gy, int gx, int &u0, int &u1) {
+        u0 = gx;
+        u1 = gx + 1;
+        if (mgrp <= 1 || (lead && gx == 0)) return;
+        const int g0 = lead + ((gx - lead) / mgrp) * mgrp;
+        const int g1 = g0 + mgrp < gw ? g0 + mgrp : gw;
+        if (g1 - g0 < 2) return;
+        const int32_t *lr = len + gy * gw, *orow = off + gy * gw;
+        const int L0 = lr[g0], o0 = orow[g0];
+        if (L0 <= 1) return;
+        for (int x = g0 + 1; x < g1; x++)
+            if (lr[x] != L0 || orow[x] != o0) return;
+        u0 = g0;
+        u1 = g1;
+    };
+    /* Cell c heads a strip of n grid rows of the unit [u0, u1); n = 0 when the cell belongs
+     * to a strip headed by another cell. */
+    auto strip_of = [&](int c, int &u0, int &u1) {
         const int gy = c / gw, gx = c - gy * gw;
-        const int o = off[c];
-        int above = 0;
-        for (int y = gy - 1; y >= 0 && len[y * gw + gx] == L && off[y * gw + gx] == o; y--) above++;
-        if (above % maxc != 0) return 0;
+        u0 = gx;
+        u1 = gx + 1;
+        if (!merge || len[c] == 1) return 1;
+        unit_of(gy, gx, u0, u1);
+        if (gx != u0) return 0;
+        const int L = len[c], o = off[c];
+        auto same = [&](int y) {
+            int a0, a1;
+            unit_of(y, gx, a0, a1);
+            return a0 == u0 && a1 == u1 && len[y * gw + gx] == L && off[y * gw + gx] == o;
+        };
+        const int blk0 = (gy / maxc) * maxc; /* strips do not cross aligned blocks of rows */
+        if (gy > blk0 && same(gy - 1)) return 0;
         int n = 1;
-        while (n < maxc && gy + n < gh && len[(gy + n) * gw + gx] == L &&
-               off[(gy + n) * gw + gx] == o)
-            n++;
+        while (gy + n < blk0 + maxc && gy + n < gh && same(gy + n)) n++;
         return n;
     };
-
-    /* rectangle s of the strip headed by cell c (n cells); false when it is empty, which
-     * happens for clipped fragments wider than FK_RECT */
-    auto sub_rect = [&](int c, int n, int s, int &rx0, int &ry0, int &fw, int &fh) {
+    /* rectangle s of the strip headed by cell c; false when it is empty, which happens for
+     * clipped fragments wider than FK_RECT */
+    auto sub_rect = [&](int c, int n, int u1, int s, int &rx0, int &ry0, int &fw, int &fh) {
         const int gy = c / gw, gx = c - gy * gw;
-        int x0, x1, y0, y1, ye0, ye1;
+        int x0, x1, y0, y1, t0, t1;
         fk_span(pd.width, F, sx, gx, x0, x1);
+        fk_span(pd.width, F, sx, u1 - 1, t0, x1);
         fk_span(pd.height, F, sy, gy, y0, y1);
-        fk_span(pd.height, F, sy, gy + n - 1, ye0, ye1);
-        (void)ye0;
-        y1 = ye1;
+        fk_span(pd.height, F, sy, gy + n - 1, t1, y1);
+        (void)t0;
+        (void)t1;
         const int sby = s / pd.nsub_x, sbx = s - sby * pd.nsub_x;
         rx0 = x0 + sbx * FK_RECT;
         ry0 = y0 + sby * FK_STRIP_ROWS;
@@ -115,10 +144,11 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     };
 
     for (int c = tid; c < ncells; c += nt) {
-        const int n = strip_cells(c);
+        int u0, u1;
+        const int n = strip_of(c, u0, u1);
         if (n == 0) continue;
         int cnt = 0, a, b2, w, h2;
-        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, s, a, b2, w, h2) ? 1 : 0;
+        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, u1, s, a, b2, w, h2) ? 1 : 0;
         if (cnt) atomicAdd(&ccount[fk_class_of(len[c])], cnt);
     }
     __syncthreads();
@@ -130,16 +160,17 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     }
     __syncthreads();
     for (int c = tid; c < ncells; c += nt) {
-        const int n = strip_cells(c);
+        int u0, u1;
+        const int n = strip_of(c, u0, u1);
         if (n == 0) continue;
         const int L = len[c];
         const int k = fk_class_of(L);
         int cnt = 0, rx0, ry0, fw, fh;
-        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, s, rx0, ry0, fw, fh) ? 1 : 0;
+        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, u1, s, rx0, ry0, fw, fh) ? 1 : 0;
         if (cnt == 0) continue;
         fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + atomicAdd(&ccount[k], cnt);
         for (int s = 0; s < per_cell; s++) {
-            if (!sub_rect(c, n, s, rx0, ry0, fw, fh)) continue;
+            if (!sub_rect(c, n, u1, s, rx0, ry0, fw, fh)) continue;
             fk_item it;
             it.frame = (uint32_t)f;
             it.xy = (uint32_t)rx0 | ((uint32_t)ry0 << 16);
