@@ -208,8 +208,8 @@ cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream
 /*
  * Render every class list of a plan.  Classes whose shortest possible filter exceeds the
  * plan's bound are empty by construction and are not launched; longest filters first.
- * h->variant: 0 = fast kernel with generic fallback, 1 = generic kernel only,
- * 2 = fast kernel without TMA.
+ * h->variant: 0 = fast kernels with generic fallback, 1 = generic kernel only,
+ * 2 = fast kernels without TMA, 3 = row-partitioned fast kernel for RGB as well.
  */
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,
@@ -223,9 +223,17 @@ cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, 
         const int class_length = fk_class_lmax(k) < bound_length ? fk_class_lmax(k) : bound_length;
         bool taken = false;
         if (h->variant != 1 && k < FK_CLASS_GENERIC) {
-            e = fk_launch_blur_fast(h, pd, k, in, out, n_frames, channels, is_f32, class_length,
-                                    s, &taken);
-            if (e != cudaSuccess) return e;
+            /* RGB: column-partitioned kernel; gray (and variant 3): row-partitioned kernel */
+            if (channels == 3 && h->variant != 3) {
+                e = fk_launch_blur_cols(h, pd, k, in, out, n_frames, is_f32, class_length, s,
+                                        &taken);
+                if (e != cudaSuccess) return e;
+            }
+            if (!taken) {
+                e = fk_launch_blur_fast(h, pd, k, in, out, n_frames, channels, is_f32,
+                                        class_length, s, &taken);
+                if (e != cudaSuccess) return e;
+            }
         }
         if (!taken) {
             e = is_f32 ? launch_generic<float>(h, pd, k, in, out, channels, class_length, s)

@@ -1,0 +1,413 @@
+/*
+ * fk_blur_cols.cu -- column-partitioned separable blur for RGB frames on sm_100a (the hot
+ * kernel of the render path).
+ *
+ * Same arithmetic as blockwise.py:136-153 (_render_cell): clamp-to-edge tile, horizontal
+ * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
+ * (convolve.py:15), taps accumulated in ascending order in fp32 -- bit-identical to
+ * fk_blur_generic and to the row-partitioned fk_blur_fast it replaces for C = 3.
+ *
+ * What is different is who does what.  A work item is a strip at most 32 pixels (96 floats)
+ * wide with one filter (fk_internal.h); a CTA of four warps walks its items 32 tile rows at
+ * a time, and WARP w OWNS THE 24 FLOAT COLUMNS [24w, 24w + 24) OF THE STRIP in both passes:
+ *
+ *   stage    the 32 x (96 + 6r) byte block arrives by TMA (128-byte x 32-row boxes from a
+ *            16-byte aligned origin); each warp converts 8 of its rows to fp32 in the shared
+ *            working tile.  [CTA barrier A: the tile is complete]
+ *   H pass   lane = tile row.  One task = the warp's 24 columns of that row: 24 accumulators,
+ *            the input window in a four-slot register ring refilled a chunk ahead
+ *            (h_task_acc, fk_stage.cuh).  The row pitch of the tile is 4 (mod 8) floats, so
+ *            the 32 rows of a warp read conflict-free.  Results go to the warp's columns of
+ *            the intermediate, which is stored TRANSPOSED (ring[column][row]): consecutive
+ *            lanes write consecutive words.  [CTA barrier B: the tile may be overwritten]
+ *   V pass   one task = one float column x 8 output rows, read from the transposed
+ *            intermediate with one LDS.128 per four rows; the 24 columns x (groups of 8 rows
+ *            that are complete) of the warp are dealt to its 32 lanes, 96 tasks = three full
+ *            rounds in the steady state.  Column pitch 4 (mod 8) floats: conflict-free.
+ *
+ * Because a warp consumes in the V pass only what it produced itself in the H pass, the
+ * intermediate needs no synchronisation at all and no slack for pipelining: it is a ring of
+ * 2r + 40 rows per column.  The only CTA-wide synchronisation left are the two barriers
+ * around the shared tile, and between them every warp has exactly the same amount of work.
+ * The next block's TMA is issued right after barrier A and lands under the H and V passes.
+ *
+ * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can touch
+ * holds a finite value so 0 * garbage never produces a NaN.
+ */
+#include "fk_stage.cuh"
+
+namespace {
+
+constexpr int kC = 3;
+constexpr int kSegF = 8 * kC;        /* float columns owned by one warp: 24 */
+constexpr int kRowF = kWarps * kSegF; /* floats per strip row: 96 */
+
+/*
+ * Vertical task on the transposed intermediate: acc[j] = sum_k g[k] * col[row0 + j + k],
+ * j < 8.  `colp` points at row 0 of the column, a ring of `cap` rows; row0 and cap are
+ * multiples of 4, so a quad of rows never straddles the wrap.  Four-slot register ring of
+ * four rows each, one LDS.128 a chunk ahead of its use.
+ */
+__device__ __forceinline__ void v_task_col(const float *__restrict__ colp, int row0, int cap,
+                                           const float *__restrict__ wts, int nchunk,
+                                           float (&acc)[kRV])
+{
+    float win[16];
+#pragma unroll
+    for (int j = 0; j < kRV; j++) acc[j] = 0.0f;
+    int rp = row0;
+#pragma unroll
+    for (int v = 0; v < 3; v++) {
+        const float4 x = *reinterpret_cast<const float4 *>(colp + rp);
+        win[4 * v + 0] = x.x;
+        win[4 * v + 1] = x.y;
+        win[4 * v + 2] = x.z;
+        win[4 * v + 3] = x.w;
+        rp += 4;
+        rp = rp >= cap ? rp - cap : rp;
+    }
+    const float4 *wp = reinterpret_cast<const float4 *>(wts);
+    float4 g4 = wp[0];
+    for (int c = 0; c < nchunk; c += 4) {
+#pragma unroll
+        for (int p = 0; p < 4; p++) {
+            if (p > 0 && c + p >= nchunk) break;
+            const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+            g4 = wp[c + p + 1]; /* next chunk's taps (one padding quad follows the last) */
+            const float4 x = *reinterpret_cast<const float4 *>(colp + rp);
+            win[(4 * (p + 3) + 0) % 16] = x.x;
+            win[(4 * (p + 3) + 1) % 16] = x.y;
+            win[(4 * (p + 3) + 2) % 16] = x.z;
+            win[(4 * (p + 3) + 3) % 16] = x.w;
+            rp += 4;
+            rp = rp >= cap ? rp - cap : rp;
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+#pragma unroll
+                for (int j = 0; j < kRV; j++)
+                    acc[j] = fmaf(g[t], win[(4 * p + t + j) % 16], acc[j]);
+            }
+        }
+    }
+}
+
+/*
+ * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
+ *              (W*3, H, N) with 128 x 32 x 1 boxes.
+ * TMA = false: plain-load staging (float32 frames, or buffers TMA cannot describe).
+ */
+template <typename T, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2)
+fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
+             const T *__restrict__ in, T *__restrict__ out, int klass, int wts_floats, int twp,
+             int npanel_max, int icap, int ipitch)
+{
+    constexpr int C = kC;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    /* layout: [raw panels][TMA barrier, 64 B][colmap][per-warp taps x 2][tile][ring] */
+    unsigned char *raw = smem_raw;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
+    int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
+    float *wts = reinterpret_cast<float *>(colmap + twp);
+    float *tile = wts + kWarps * 2 * wts_floats;
+    float *ring = tile + kTB * twp; /* [kRowF columns][ipitch], icap rows used */
+
+    const int W = pd.width, H = pd.height;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
+    const int n_items = pd.counters[klass];
+    const int stride = (int)gridDim.x;
+    const uint4 none = make_uint4(0u, 0u, 0u, 0u);
+    auto load_item = [&](int i) {
+        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
+    };
+    /* One 32-row block of an item: the box origin is clamped into the image so that every
+     * clamped source row / column of the block lies inside the box. */
+    auto issue = [&](const item_geo &g, int rb) {
+        const int c0a = (g.xs_c * C) & ~15;
+        const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
+        mbar_expect_tx(bar, (uint32_t)(g.npanel * kPanelBytes));
+        for (int p = 0; p < g.npanel; p++)
+            tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
+    };
+    /* Zero-padded taps of an item into one of THIS WARP's two tap buffers with cp.async
+     * (src-size 0 writes the zero padding). */
+    auto fill_taps = [&](const uint4 q, int slot) {
+        const int L = (int)((q.z >> 8) & 0x1fffu);
+        const int n = 4 * ((L + 3) >> 2) + 4;
+        const float *taps = pd.taps + q.w;
+        float *dst = wts + (warp * 2 + slot) * wts_floats;
+        for (int i = lane; i < n; i += 32) {
+            const int in_range = i < L;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
+                         "l"(taps + (in_range ? i : 0)), "r"(in_range ? 4 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    int idx = (int)blockIdx.x;
+    uint4 q_cur = load_item(idx);
+    uint4 q_nxt = load_item(idx + stride);
+    if (TMA && tid == 0) mbar_init(bar, 1);
+    /* rows of the intermediate a padded tap can reach before they have been produced must
+     * hold finite values, so start from zeros */
+    for (int i = tid; i < kRowF * ipitch / 4; i += kThreads)
+        reinterpret_cast<float4 *>(ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (idx < n_items) fill_taps(q_cur, 0);
+    __syncthreads();
+    if (TMA && tid == 0 && idx < n_items) issue(decode_item<C>(q_cur, W), 0);
+
+    uint32_t phase = 0;
+    int wslot = 0;
+    uint4 q_nn = none;
+    for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wslot ^= 1) {
+        q_nn = load_item(idx + 2 * stride); /* descriptor prefetch, two items ahead */
+        const bool have_next = idx + stride < n_items;
+        const float *w_cur = wts + (warp * 2 + wslot) * wts_floats;
+        /* this item's taps were requested one item ago by this warp */
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        /* request the next item's: that buffer held the previous item's taps */
+        if (have_next) fill_taps(q_nxt, wslot ^ 1);
+
+        const item_geo g = decode_item<C>(q_cur, W);
+        const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
+        const int nchunk = g.nchunk, th = g.th, tw = g.tw, twz = g.twz;
+        const size_t frame_off = (size_t)g.f * H * W * C;
+        const T *src = in + frame_off;
+        T *dst = out + frame_off;
+        const bool vec = TMA && g.xin; /* vector converter, no column map */
+        const int ncol = fw * C - kSegF * warp < kSegF ? fw * C - kSegF * warp : kSegF;
+        const bool active = ncol > 0; /* this warp owns columns of this item */
+
+        if (vec) {
+            /* the vector converter writes whole quads up to tw only; the tile columns
+             * beyond, which only padded taps and discarded outputs touch, are zeroed once
+             * per item by the warp that owns the rows */
+            const int q0 = (tw + 3) >> 2, nq = (twz >> 2) - q0;
+            for (int i = lane; i < nq * kWR; i += 32) {
+                const int row = i / nq, q = i - row * nq;
+                reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[q0 + q] =
+                    make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        } else {
+            /* clamp-to-edge by index.  TMA: tile column -> byte offset inside the box; plain
+             * loads: tile column -> element offset inside the image row.  Everybody is past
+             * the last barrier of the previous item, so nobody reads the old map any more. */
+            for (int j = tid; j < twz; j += kThreads) {
+                int m = -1;
+                if (j < tw) {
+                    const int px = j / C, c = j - px * C;
+                    const int xx = fast_clamp(x0 - r + px, 0, W - 1);
+                    if (TMA) {
+                        m = g.skew + (xx - g.xs_c) * C + c;
+                        m = (m >> 7) * kPanelBytes + (m & (kPanelB - 1));
+                    } else {
+                        m = xx * C + c;
+                    }
+                }
+                colmap[j] = m;
+            }
+            __syncthreads();
+        }
+
+        const int ngroups = (fh + kRV - 1) / kRV; /* groups of 8 output rows */
+        const int nblk = (th + kTB - 1) / kTB;
+        int vdone = 0; /* output groups rendered so far */
+        int rbm = 0;   /* ring row of the first tile row of the block */
+        for (int b = 0; b < nblk; b++) {
+            const int rb = b * kTB;
+            const int nrows = th - rb < kTB ? th - rb : kTB;
+            const int ys = y0 - r + rb;
+            const bool mine = warp * kWR < nrows; /* this warp converts rows of this block */
+            if (TMA) {
+                mbar_wait(bar, phase);
+                phase ^= 1;
+                if (mine) {
+                    const int ys_c = fast_clamp(ys, 0, H - 1);
+                    if (vec) {
+                        const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
+                        const int bsh = (g.skew & 3) * 8;
+                        const int w0 = lane + (g.skew >> 2), w1 = w0 + 1;
+                        const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
+                        const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
+                        const int nw = (tw + 3) >> 2;
+                        const int np = (nw + 31) >> 5;
+                        bool pred[kMaxPanels - 1];
+#pragma unroll
+                        for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
+                        float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp) + lane;
+                        if (ys >= 0 && ys + kTB <= H) {
+                            const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
+                            const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
+                            switch (np) {
+                            case 1: convert_rows_vec<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            case 2: convert_rows_vec<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            case 3: convert_rows_vec<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            default: convert_rows_vec<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                            }
+                        } else { /* rows clamp at the top / bottom edge of the image */
+                            for (int i = 0; i < kWR; i++) {
+                                const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
+                                const uint32_t *rp = raw32 + rr * (kPanelB / 4);
+#pragma unroll
+                                for (int p = 0; p < kMaxPanels - 1; p++) {
+                                    if (pred[p]) {
+                                        const uint32_t lo = rp[i0 + p * kPanelWords];
+                                        const uint32_t hi = rp[i1 + p * kPanelWords];
+                                        tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                    }
+                                }
+                                tp += twp / 4;
+                            }
+                        }
+                    } else {
+                        for (int i = 0; i < kWR; i++) {
+                            const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
+                            const unsigned char *rp = raw + rr * kPanelB;
+                            float *tp = tile + (warp * kWR + i) * twp;
+                            for (int j = lane; j < twz; j += 32) {
+                                const int m = colmap[j];
+                                tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
+                            }
+                        }
+                    }
+                }
+            } else if (mine) {
+                /* plain loads, eight rows in flight per lane */
+                const T *grow[kWR];
+#pragma unroll
+                for (int i = 0; i < kWR; i++)
+                    grow[i] = src + (size_t)fast_clamp(ys + warp * kWR + i, 0, H - 1) * W * C;
+                float *tp = tile + warp * kWR * twp;
+                for (int j = lane; j < twz; j += 32) {
+                    const int m = colmap[j];
+                    float v[kWR];
+#pragma unroll
+                    for (int i = 0; i < kWR; i++) v[i] = m >= 0 ? fast_px<T>::load(grow[i] + m) : 0.0f;
+#pragma unroll
+                    for (int i = 0; i < kWR; i++) tp[i * twp + j] = v[i];
+                }
+            }
+            __syncthreads(); /* A: the tile is complete and the raw bytes are free */
+            if (TMA && tid == 0) {
+                if (rb + kTB < th)
+                    issue(g, rb + kTB);
+                else if (have_next)
+                    issue(decode_item<C>(q_nxt, W), 0);
+            }
+
+            /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns */
+            if (active && lane < nrows) {
+                float acc[kSegF];
+                h_task_acc<C>(tile + lane * twp + kSegF * warp, w_cur, nchunk, acc);
+                int rr = rbm + lane;
+                rr = rr >= icap ? rr - icap : rr;
+                float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
+#pragma unroll
+                for (int j = 0; j < kSegF; j++) rp[j * ipitch] = acc[j];
+            }
+            rbm += kTB;
+            while (rbm >= icap) rbm -= icap;
+            __syncthreads(); /* B: the tile may be overwritten; also orders H before V */
+
+            /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over the output
+             * groups whose 8 + 2r intermediate rows exist now */
+            const int produced = rb + nrows;
+            int jend = ngroups;
+            if (produced < th) {
+                const int avail = produced - 2 * r - kRV;
+                jend = avail >= 0 ? avail / kRV + 1 : 0;
+                jend = jend < ngroups ? jend : ngroups;
+            }
+            if (active) {
+                const int ntask = (jend - vdone) * kSegF;
+                for (int t = lane; t < ntask; t += 32) {
+                    const int gq = t / kSegF;
+                    const int col = t - gq * kSegF;
+                    const int gi = vdone + gq;
+                    if (col < ncol) {
+                        int r0 = gi * kRV;
+                        while (r0 >= icap) r0 -= icap;
+                        float acc[kRV];
+                        v_task_col(ring + (size_t)(kSegF * warp + col) * ipitch, r0, icap, w_cur,
+                                   nchunk, acc);
+                        T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + col;
+#pragma unroll
+                        for (int j = 0; j < kRV; j++) {
+                            if (gi * kRV + j < fh) *op = fast_px<T>::store(acc[j]);
+                            op += (size_t)W * C;
+                        }
+                    }
+                }
+            }
+            vdone = jend;
+        }
+    }
+}
+
+struct cols_layout {
+    int wts_floats, twp, icap, ipitch, npanel;
+    size_t smem;
+};
+
+cols_layout cols_layout_for(int max_length, bool tma)
+{
+    cols_layout l;
+    const int nchunk = (max_length + 3) / 4;
+    const int r = (max_length - 1) / 2;
+    l.wts_floats = 4 * nchunk + 4; /* one zero quad after the last chunk (tap prefetch) */
+    const int twz = kC * (8 * kWarps + 4 + 4 * nchunk);
+    int twp = (twz + 3) & ~3;
+    if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
+    l.twp = twp;
+    l.icap = (2 * r + 40 + 7) & ~7; /* see the header: no slack needed */
+    l.ipitch = l.icap + 4;          /* 4 (mod 8) floats */
+    l.npanel = tma ? (15 + (kSub + 2 * r) * kC + 4 + kPanelB - 1) / kPanelB : 0;
+    l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)twp * sizeof(int) +
+             ((size_t)kWarps * 2 * l.wts_floats + (size_t)kTB * twp + (size_t)kRowF * l.ipitch) *
+                 sizeof(float);
+    return l;
+}
+
+template <typename T, bool TMA>
+cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev &pd, int klass,
+                        const void *in, void *out, int class_length, cudaStream_t s, bool *taken)
+{
+    const cols_layout l = cols_layout_for(class_length, TMA);
+    *taken = false;
+    const size_t max_smem = h->prop.sharedMemPerBlockOptin;
+    if (l.smem > max_smem || (TMA && l.npanel > kMaxPanels)) return cudaSuccess;
+    auto kernel = fk_blur_cols<T, TMA>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)l.smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, l.smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaSuccess;
+    const int grid = h->prop.multiProcessorCount * occ;
+    kernel<<<grid, kThreads, l.smem, s>>>(map, pd, (const T *)in, (T *)out, klass, l.wts_floats,
+                                          l.twp, l.npanel, l.icap, l.ipitch);
+    *taken = true;
+    return cudaGetLastError();
+}
+
+} // namespace
+
+/* Renders the items of one class list of an RGB batch.  Returns cudaSuccess with
+ * *taken = false when the kernel cannot take the class (filters too long for its
+ * shared-memory layout).  h->variant 2 = plain-load staging (no TMA). */
+cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
+                                void *out, int n_frames, int is_f32, int class_length,
+                                cudaStream_t s, bool *taken)
+{
+    CUtensorMap map;
+    memset(&map, 0, sizeof map);
+    if (is_f32) return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
+    const bool tma = h->variant != 2 && make_tensor_map(&map, in, pd.width, pd.height, kC, n_frames);
+    if (tma) return launch_cols<uint8_t, true>(h, map, pd, klass, in, out, class_length, s, taken);
+    return launch_cols<uint8_t, false>(h, map, pd, klass, in, out, class_length, s, taken);
+}

@@ -154,6 +154,9 @@ cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, 
 cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
                                 void *out, int n_frames, int channels, int is_f32,
                                 int class_length, cudaStream_t s, bool *taken);
+cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
+                                void *out, int n_frames, int is_f32, int class_length,
+                                cudaStream_t s, bool *taken);
 cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s);
 
 /* Host replica of the grid geometry (tiling.py:15-28). */
