@@ -31,6 +31,13 @@
  * around the shared tile, and between them every warp has exactly the same amount of work.
  * The next block's TMA is issued right after barrier A and lands under the H and V passes.
  *
+ * Long filters: the working tile is what limits the CTAs per SM, so for the classes with
+ * long filters the taps are walked in up to four PANELS of `pc` chunks.  Panel p needs only
+ * the tile columns [12 pc p, 12 pc (p + 1) + 96 + ...), so the tile is as wide as one panel;
+ * the raw bytes of the block stay in shared memory and are converted panel by panel, the 24
+ * accumulators of a lane's row stay in registers across panels (same taps, same order: the
+ * result does not change), and each panel costs one more pair of barriers.
+ *
  * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can touch
  * holds a finite value so 0 * garbage never produces a NaN.
  */
@@ -42,50 +49,150 @@ constexpr int kC = 3;
 constexpr int kSegF = 8 * kC;        /* float columns owned by one warp: 24 */
 constexpr int kRowF = kWarps * kSegF; /* floats per strip row: 96 */
 
-/*
- * Vertical task on the transposed intermediate: acc[j] = sum_k g[k] * col[row0 + j + k],
- * j < 8.  `colp` points at row 0 of the column, a ring of `cap` rows; row0 and cap are
- * multiples of 4, so a quad of rows never straddles the wrap.  Four-slot register ring of
- * four rows each, one LDS.128 a chunk ahead of its use.
- */
-__device__ __forceinline__ void v_task_col(const float *__restrict__ colp, int row0, int cap,
-                                           const float *__restrict__ wts, int nchunk,
-                                           float (&acc)[kRV])
+__device__ __forceinline__ float4 lds128(uint32_t addr)
 {
-    float win[16];
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
+/*
+ * Horizontal task, one panel of taps: acc[j] += sum_k g[k] * in[j + 3k], j in [0, 24), for
+ * one tile row.  `trow` is the shared address of the first input float of the warp's
+ * columns for this panel (16-byte aligned), `wts` of the panel's first tap; nchunk chunks of
+ * four taps.  Ring of four slots of 12 input values: a chunk reads slots p, p+1, p+2 and
+ * refills slot p+3 -- dead since the previous chunk -- with the values the NEXT chunk needs.
+ * Whole turns of the ring first, then the last one to three chunks.
+ */
+__device__ __forceinline__ void h_part(uint32_t trow, uint32_t wts, int nchunk,
+                                       float (&acc)[kSegF])
+{
+    constexpr int C = kC, NW = 16 * C;
+    float win[NW];
 #pragma unroll
-    for (int j = 0; j < kRV; j++) acc[j] = 0.0f;
-    int rp = row0;
-#pragma unroll
-    for (int v = 0; v < 3; v++) {
-        const float4 x = *reinterpret_cast<const float4 *>(colp + rp);
+    for (int v = 0; v < 3 * C; v++) {
+        const float4 x = lds128(trow + 16 * v);
         win[4 * v + 0] = x.x;
         win[4 * v + 1] = x.y;
         win[4 * v + 2] = x.z;
         win[4 * v + 3] = x.w;
-        rp += 4;
-        rp = rp >= cap ? rp - cap : rp;
     }
-    const float4 *wp = reinterpret_cast<const float4 *>(wts);
-    float4 g4 = wp[0];
-    for (int c = 0; c < nchunk; c += 4) {
+    uint32_t nxt = trow + 16 * 3 * C;
+    float4 g4 = lds128(wts);
+    uint32_t wa = wts + 16;
+    auto chunk = [&](const int p) {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa); /* next chunk's taps (a quad always follows: next panel or padding) */
+        wa += 16;
 #pragma unroll
-        for (int p = 0; p < 4; p++) {
-            if (p > 0 && c + p >= nchunk) break;
-            const float g[4] = {g4.x, g4.y, g4.z, g4.w};
-            g4 = wp[c + p + 1]; /* next chunk's taps (one padding quad follows the last) */
-            const float4 x = *reinterpret_cast<const float4 *>(colp + rp);
-            win[(4 * (p + 3) + 0) % 16] = x.x;
-            win[(4 * (p + 3) + 1) % 16] = x.y;
-            win[(4 * (p + 3) + 2) % 16] = x.z;
-            win[(4 * (p + 3) + 3) % 16] = x.w;
-            rp += 4;
-            rp = rp >= cap ? rp - cap : rp;
+        for (int v = 0; v < C; v++) {
+            const float4 x = lds128(nxt + 16 * v);
+            const int q = (((p + 3) % 4) * C + v) * 4;
+            win[q + 0] = x.x;
+            win[q + 1] = x.y;
+            win[q + 2] = x.z;
+            win[q + 3] = x.w;
+        }
+        nxt += 16 * C;
 #pragma unroll
-            for (int t = 0; t < 4; t++) {
+        for (int t = 0; t < 4; t++) {
 #pragma unroll
-                for (int j = 0; j < kRV; j++)
-                    acc[j] = fmaf(g[t], win[(4 * p + t + j) % 16], acc[j]);
+            for (int j = 0; j < kSegF; j++)
+                acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
+        }
+    };
+    int c = 0;
+    for (; c + 4 <= nchunk; c += 4) {
+        chunk(0);
+        chunk(1);
+        chunk(2);
+        chunk(3);
+    }
+    if (c < nchunk) {
+        chunk(0);
+        if (c + 1 < nchunk) {
+            chunk(1);
+            if (c + 2 < nchunk) chunk(2);
+        }
+    }
+}
+
+/*
+ * Vertical task on the transposed intermediate: acc[j] = sum_k g[k] * col[row0 + j + k],
+ * j < 8.  `col` is the shared-memory address of row 0 of the column, a ring of `cap` rows;
+ * row0 and cap are multiples of 4, so a quad of rows never straddles the wrap.  Four-slot
+ * register ring of four rows each, one LDS.128 a chunk ahead of its use.  The chunk loop
+ * runs whole turns of the ring (no exit inside the unrolled body) and then the last one
+ * to three chunks; addresses are raw 32-bit shared addresses so that stepping and wrapping
+ * cost three integer instructions per chunk.
+ */
+__device__ __forceinline__ void v_task_col(uint32_t col, int row0, int cap, uint32_t wts,
+                                           int nchunk, float (&acc)[kRV])
+{
+    float win[16];
+#pragma unroll
+    for (int j = 0; j < kRV; j++) acc[j] = 0.0f;
+    const uint32_t end = col + 4u * (uint32_t)cap;
+    uint32_t a = col + 4u * (uint32_t)row0;
+#pragma unroll
+    for (int v = 0; v < 3; v++) {
+        const float4 x = lds128(a);
+        win[4 * v + 0] = x.x;
+        win[4 * v + 1] = x.y;
+        win[4 * v + 2] = x.z;
+        win[4 * v + 3] = x.w;
+        a += 16;
+        a = a == end ? col : a;
+    }
+    float4 g4 = lds128(wts);
+    uint32_t wa = wts + 16;
+    /* one chunk of four taps at ring phase p; `la` = address of the quad of rows to load */
+    auto chunk = [&](const int p, const uint32_t la) {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
+        wa += 16;
+        const float4 x = lds128(la);
+        win[(4 * (p + 3) + 0) % 16] = x.x;
+        win[(4 * (p + 3) + 1) % 16] = x.y;
+        win[(4 * (p + 3) + 2) % 16] = x.z;
+        win[(4 * (p + 3) + 3) % 16] = x.w;
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+#pragma unroll
+            for (int j = 0; j < kRV; j++)
+                acc[j] = fmaf(g[t], win[(4 * p + t + j) % 16], acc[j]);
+        }
+    };
+    auto step = [&](uint32_t x) {
+        x += 16;
+        return x == end ? col : x;
+    };
+    int c = 0;
+    for (; c + 4 <= nchunk; c += 4) {
+        /* the four load addresses of this turn: plain offsets unless the ring wraps in it */
+        uint32_t a1 = a + 16, a2 = a + 32, a3 = a + 48, an = a + 64;
+        if (an >= end) {
+            a1 = step(a);
+            a2 = step(a1);
+            a3 = step(a2);
+            an = step(a3);
+        }
+        chunk(0, a);
+        chunk(1, a1);
+        chunk(2, a2);
+        chunk(3, a3);
+        a = an;
+    }
+    if (c < nchunk) {
+        chunk(0, a);
+        if (c + 1 < nchunk) {
+            a = step(a);
+            chunk(1, a);
+            if (c + 2 < nchunk) {
+                a = step(a);
+                chunk(2, a);
             }
         }
     }
@@ -100,17 +207,20 @@ template <typename T, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
 fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
              const T *__restrict__ in, T *__restrict__ out, int klass, int wts_floats, int twp,
-             int npanel_max, int icap, int ipitch)
+             int npanel_max, int icap, int ipitch, int cmw, int pc)
 {
+    /* twp: pitch of the working tile (one panel wide); cmw: ints in the column map (full
+     * tile width); pc: chunks of four taps per panel */
     constexpr int C = kC;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     /* layout: [raw panels][TMA barrier, 64 B][colmap][per-warp taps x 2][tile][ring] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
     int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
-    float *wts = reinterpret_cast<float *>(colmap + twp);
+    float *wts = reinterpret_cast<float *>(colmap + cmw);
     float *tile = wts + kWarps * 2 * wts_floats;
     float *ring = tile + kTB * twp; /* [kRowF columns][ipitch], icap rows used */
+    const uint32_t ring_s = smem_u32(ring), tile_s = smem_u32(tile);
 
     const int W = pd.width, H = pd.height;
     const int tid = threadIdx.x;
@@ -182,17 +292,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const int ncol = fw * C - kSegF * warp < kSegF ? fw * C - kSegF * warp : kSegF;
         const bool active = ncol > 0; /* this warp owns columns of this item */
 
-        if (vec) {
-            /* the vector converter writes whole quads up to tw only; the tile columns
-             * beyond, which only padded taps and discarded outputs touch, are zeroed once
-             * per item by the warp that owns the rows */
-            const int q0 = (tw + 3) >> 2, nq = (twz >> 2) - q0;
-            for (int i = lane; i < nq * kWR; i += 32) {
-                const int row = i / nq, q = i - row * nq;
-                reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[q0 + q] =
-                    make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        } else {
+        if (!vec) {
             /* clamp-to-edge by index.  TMA: tile column -> byte offset inside the box; plain
              * loads: tile column -> element offset inside the image row.  Everybody is past
              * the last barrier of the previous item, so nobody reads the old map any more. */
@@ -215,6 +315,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 
         const int ngroups = (fh + kRV - 1) / kRV; /* groups of 8 output rows */
         const int nblk = (th + kTB - 1) / kTB;
+        const int npan = (nchunk + pc - 1) / pc;  /* tap panels of this item */
         int vdone = 0; /* output groups rendered so far */
         int rbm = 0;   /* ring row of the first tile row of the block */
         for (int b = 0; b < nblk; b++) {
@@ -222,96 +323,122 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             const int nrows = th - rb < kTB ? th - rb : kTB;
             const int ys = y0 - r + rb;
             const bool mine = warp * kWR < nrows; /* this warp converts rows of this block */
-            if (TMA) {
-                mbar_wait(bar, phase);
-                phase ^= 1;
-                if (mine) {
-                    const int ys_c = fast_clamp(ys, 0, H - 1);
-                    if (vec) {
-                        const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
-                        const int bsh = (g.skew & 3) * 8;
-                        const int w0 = lane + (g.skew >> 2), w1 = w0 + 1;
-                        const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
-                        const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
-                        const int nw = (tw + 3) >> 2;
-                        const int np = (nw + 31) >> 5;
-                        bool pred[kMaxPanels - 1];
+            float hacc[kSegF];
 #pragma unroll
-                        for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
-                        float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp) + lane;
-                        if (ys >= 0 && ys + kTB <= H) {
-                            const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
-                            const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
-                            switch (np) {
-                            case 1: convert_rows_vec<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                            case 2: convert_rows_vec<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                            case 3: convert_rows_vec<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                            default: convert_rows_vec<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+            for (int j = 0; j < kSegF; j++) hacc[j] = 0.0f;
+            for (int pn = 0; pn < npan; pn++) {
+                const int c0 = pn * pc;
+                const int nch = nchunk - c0 < pc ? nchunk - c0 : pc;
+                const int f0 = 4 * C * c0;                        /* first tile float of the panel */
+                const int pwz = C * (8 * g.nseg + 4 + 4 * nch);   /* floats the H tasks may touch */
+                const int pval = tw - f0 < pwz ? tw - f0 : pwz;   /* of which image data */
+                if (TMA) {
+                    if (pn == 0) {
+                        mbar_wait(bar, phase);
+                        phase ^= 1;
+                    }
+                    if (mine) {
+                        const int ys_c = fast_clamp(ys, 0, H - 1);
+                        if (vec) {
+                            const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
+                            const int sk = g.skew + f0; /* raw byte of the panel's first float */
+                            const int bsh = (sk & 3) * 8;
+                            const int w0 = lane + (sk >> 2), w1 = w0 + 1;
+                            const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
+                            const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
+                            const int nw = (pval + 3) >> 2; /* quads with image data */
+                            const int np = (nw + 31) >> 5;
+                            bool pred[kMaxPanels - 1];
+#pragma unroll
+                            for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
+                            float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp) + lane;
+                            if (ys >= 0 && ys + kTB <= H) {
+                                const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
+                                const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
+                                switch (np) {
+                                case 1: convert_rows_vec<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                case 2: convert_rows_vec<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                case 3: convert_rows_vec<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                default: convert_rows_vec<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                }
+                            } else { /* rows clamp at the top / bottom edge of the image */
+                                for (int i = 0; i < kWR; i++) {
+                                    const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
+                                    const uint32_t *rp = raw32 + rr * (kPanelB / 4);
+#pragma unroll
+                                    for (int p = 0; p < kMaxPanels - 1; p++) {
+                                        if (pred[p]) {
+                                            const uint32_t lo = rp[i0 + p * kPanelWords];
+                                            const uint32_t hi = rp[i1 + p * kPanelWords];
+                                            tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                        }
+                                    }
+                                    tp += twp / 4;
+                                }
                             }
-                        } else { /* rows clamp at the top / bottom edge of the image */
+                            /* the vector converter writes whole quads of image data only; the
+                             * columns beyond, which only padded taps and discarded outputs
+                             * touch, are zeroed -- once per item, or every time when panels
+                             * of different widths share the tile */
+                            if (b == 0 || npan > 1) {
+                                const int nq = (pwz >> 2) - nw;
+                                for (int i = lane; i < nq * kWR; i += 32) {
+                                    const int row = i / nq, q = i - row * nq;
+                                    reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[nw + q] =
+                                        make_float4(0.f, 0.f, 0.f, 0.f);
+                                }
+                            }
+                        } else {
                             for (int i = 0; i < kWR; i++) {
                                 const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
-                                const uint32_t *rp = raw32 + rr * (kPanelB / 4);
-#pragma unroll
-                                for (int p = 0; p < kMaxPanels - 1; p++) {
-                                    if (pred[p]) {
-                                        const uint32_t lo = rp[i0 + p * kPanelWords];
-                                        const uint32_t hi = rp[i1 + p * kPanelWords];
-                                        tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
-                                    }
+                                const unsigned char *rp = raw + rr * kPanelB;
+                                float *tp = tile + (warp * kWR + i) * twp;
+                                for (int j = lane; j < pwz; j += 32) {
+                                    const int m = f0 + j < twz ? colmap[f0 + j] : -1;
+                                    tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
                                 }
-                                tp += twp / 4;
-                            }
-                        }
-                    } else {
-                        for (int i = 0; i < kWR; i++) {
-                            const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
-                            const unsigned char *rp = raw + rr * kPanelB;
-                            float *tp = tile + (warp * kWR + i) * twp;
-                            for (int j = lane; j < twz; j += 32) {
-                                const int m = colmap[j];
-                                tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
                             }
                         }
                     }
+                } else if (mine) {
+                    /* plain loads, eight rows in flight per lane */
+                    const T *grow[kWR];
+#pragma unroll
+                    for (int i = 0; i < kWR; i++)
+                        grow[i] = src + (size_t)fast_clamp(ys + warp * kWR + i, 0, H - 1) * W * C;
+                    float *tp = tile + warp * kWR * twp;
+                    for (int j = lane; j < pwz; j += 32) {
+                        const int m = f0 + j < twz ? colmap[f0 + j] : -1;
+                        float v[kWR];
+#pragma unroll
+                        for (int i = 0; i < kWR; i++)
+                            v[i] = m >= 0 ? fast_px<T>::load(grow[i] + m) : 0.0f;
+#pragma unroll
+                        for (int i = 0; i < kWR; i++) tp[i * twp + j] = v[i];
+                    }
                 }
-            } else if (mine) {
-                /* plain loads, eight rows in flight per lane */
-                const T *grow[kWR];
-#pragma unroll
-                for (int i = 0; i < kWR; i++)
-                    grow[i] = src + (size_t)fast_clamp(ys + warp * kWR + i, 0, H - 1) * W * C;
-                float *tp = tile + warp * kWR * twp;
-                for (int j = lane; j < twz; j += 32) {
-                    const int m = colmap[j];
-                    float v[kWR];
-#pragma unroll
-                    for (int i = 0; i < kWR; i++) v[i] = m >= 0 ? fast_px<T>::load(grow[i] + m) : 0.0f;
-#pragma unroll
-                    for (int i = 0; i < kWR; i++) tp[i * twp + j] = v[i];
+                __syncthreads(); /* A: the tile holds the panel */
+                if (TMA && tid == 0 && pn == npan - 1) { /* the raw bytes are free */
+                    if (rb + kTB < th)
+                        issue(g, rb + kTB);
+                    else if (have_next)
+                        issue(decode_item<C>(q_nxt, W), 0);
                 }
-            }
-            __syncthreads(); /* A: the tile is complete and the raw bytes are free */
-            if (TMA && tid == 0) {
-                if (rb + kTB < th)
-                    issue(g, rb + kTB);
-                else if (have_next)
-                    issue(decode_item<C>(q_nxt, W), 0);
-            }
-
-            /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns */
-            if (active && lane < nrows) {
-                float acc[kSegF];
-                h_task_acc<C>(tile + lane * twp + kSegF * warp, w_cur, nchunk, acc);
-                int rr = rbm + lane;
-                rr = rr >= icap ? rr - icap : rr;
-                float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
+                /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns */
+                if (active && lane < nrows)
+                    h_part(tile_s + 4u * (uint32_t)(lane * twp + kSegF * warp),
+                           smem_u32(w_cur) + 16u * (uint32_t)c0, nch, hacc);
+                if (pn == npan - 1 && active && lane < nrows) {
+                    int rr = rbm + lane;
+                    rr = rr >= icap ? rr - icap : rr;
+                    float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
 #pragma unroll
-                for (int j = 0; j < kSegF; j++) rp[j * ipitch] = acc[j];
+                    for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
+                }
+                __syncthreads(); /* B: the tile may be overwritten; also orders H before V */
             }
             rbm += kTB;
             while (rbm >= icap) rbm -= icap;
-            __syncthreads(); /* B: the tile may be overwritten; also orders H before V */
 
             /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over the output
              * groups whose 8 + 2r intermediate rows exist now */
@@ -332,8 +459,8 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         int r0 = gi * kRV;
                         while (r0 >= icap) r0 -= icap;
                         float acc[kRV];
-                        v_task_col(ring + (size_t)(kSegF * warp + col) * ipitch, r0, icap, w_cur,
-                                   nchunk, acc);
+                        v_task_col(ring_s + 4u * (uint32_t)((kSegF * warp + col) * ipitch), r0, icap,
+                                   smem_u32(w_cur), nchunk, acc);
                         T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + col;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
@@ -349,24 +476,27 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 }
 
 struct cols_layout {
-    int wts_floats, twp, icap, ipitch, npanel;
+    int wts_floats, twp, icap, ipitch, npanel, cmw, pc;
     size_t smem;
 };
 
-cols_layout cols_layout_for(int max_length, bool tma)
+/* Shared-memory layout for filters up to max_length walked in `npan` tap panels. */
+cols_layout cols_layout_for(int max_length, bool tma, int npan)
 {
     cols_layout l;
     const int nchunk = (max_length + 3) / 4;
     const int r = (max_length - 1) / 2;
+    l.pc = (nchunk + npan - 1) / npan;
     l.wts_floats = 4 * nchunk + 4; /* one zero quad after the last chunk (tap prefetch) */
-    const int twz = kC * (8 * kWarps + 4 + 4 * nchunk);
+    const int twz = kC * (8 * kWarps + 4 + 4 * l.pc); /* one panel */
     int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
-    l.icap = (2 * r + 40 + 7) & ~7; /* see the header: no slack needed */
-    l.ipitch = l.icap + 4;          /* 4 (mod 8) floats */
+    l.cmw = (kC * (8 * kWarps + 4 + 4 * nchunk) + 3) & ~3; /* column map: the full width */
+    l.icap = (2 * r + 40 + 3) & ~3; /* see the header: no slack needed */
+    l.ipitch = (l.icap & 7) == 4 ? l.icap : l.icap + 4; /* 4 (mod 8) floats */
     l.npanel = tma ? (15 + (kSub + 2 * r) * kC + 4 + kPanelB - 1) / kPanelB : 0;
-    l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)twp * sizeof(int) +
+    l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)l.cmw * sizeof(int) +
              ((size_t)kWarps * 2 * l.wts_floats + (size_t)kTB * twp + (size_t)kRowF * l.ipitch) *
                  sizeof(float);
     return l;
@@ -376,9 +506,22 @@ template <typename T, bool TMA>
 cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev &pd, int klass,
                         const void *in, void *out, int class_length, cudaStream_t s, bool *taken)
 {
-    const cols_layout l = cols_layout_for(class_length, TMA);
     *taken = false;
     const size_t max_smem = h->prop.sharedMemPerBlockOptin;
+    /* two CTAs per SM when up to four tap panels make the layout fit, else one */
+    const size_t per_sm = h->prop.sharedMemPerMultiprocessor;
+    const size_t reserved = h->prop.reservedSharedMemPerBlock;
+    const size_t two_cta = per_sm / 2 > reserved ? per_sm / 2 - reserved : 0;
+    cols_layout l = cols_layout_for(class_length, TMA, 1);
+    if (l.smem > two_cta) {
+        for (int np = 2; np <= 4; np++) {
+            const cols_layout c = cols_layout_for(class_length, TMA, np);
+            if (c.smem <= two_cta) {
+                l = c;
+                break;
+            }
+        }
+    }
     if (l.smem > max_smem || (TMA && l.npanel > kMaxPanels)) return cudaSuccess;
     auto kernel = fk_blur_cols<T, TMA>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -390,7 +533,7 @@ cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     if (occ < 1) return cudaSuccess;
     const int grid = h->prop.multiProcessorCount * occ;
     kernel<<<grid, kThreads, l.smem, s>>>(map, pd, (const T *)in, (T *)out, klass, l.wts_floats,
-                                          l.twp, l.npanel, l.icap, l.ipitch);
+                                          l.twp, l.npanel, l.icap, l.ipitch, l.cmw, l.pc);
     *taken = true;
     return cudaGetLastError();
 }
