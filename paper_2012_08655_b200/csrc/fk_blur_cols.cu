@@ -59,6 +59,79 @@ __device__ __forceinline__ float4 lds128(uint32_t addr)
 }
 
 /*
+ * uint8 frames: byte -> fp32 without an arithmetic instruction.  The word (b << 16) read as a
+ * float IS b * 2^-133 for every b in [0, 255]: below 2^24 the float encoding is linear
+ * (the denormals and the first normal binade share one spacing), so one PRMT per byte makes
+ * an exact input value.  The horizontal taps are scaled by 2^120 when a warp fetches them,
+ * which puts the intermediate at 2^-13 of its true value -- every FMA rounds exactly as the
+ * unscaled one does (powers of two; nothing is near under- or overflow), so the result is
+ * still bit-identical to fk_blur_generic -- and the 2^13 comes back for free in the FMA that
+ * adds the rounding half before the store.  float32 frames use the values as they are.
+ */
+constexpr float kTapScaleH = 1.329227995784916e36f; /* 2^120 */
+constexpr float kOutScale = 8192.0f;                /* 2^13 */
+
+__device__ __forceinline__ float4 bytes_to_float4_s(uint32_t w)
+{
+    float4 f;
+    f.x = __uint_as_float(__byte_perm(w, 0u, 0x4044));
+    f.y = __uint_as_float(__byte_perm(w, 0u, 0x4144));
+    f.z = __uint_as_float(__byte_perm(w, 0u, 0x4244));
+    f.w = __uint_as_float(__byte_perm(w, 0u, 0x4344));
+    return f;
+}
+template <typename T> struct cols_px;
+template <> struct cols_px<uint8_t> {
+    static __device__ __forceinline__ float load(const uint8_t *p)
+    {
+        return __uint_as_float((uint32_t)__ldg(p) << 16);
+    }
+    static __device__ __forceinline__ float from_byte(unsigned char b)
+    {
+        return __uint_as_float((uint32_t)b << 16);
+    }
+    static __device__ __forceinline__ uint8_t store(float v)
+    {
+        /* convolve.py:15: clip(floor(v + 0.5), 0, 255); cvt.rmi saturates to [0, 255] */
+        uint32_t u;
+        asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(u) : "f"(fmaf(v, kOutScale, 0.5f)));
+        return (uint8_t)u;
+    }
+};
+template <> struct cols_px<float> {
+    static __device__ __forceinline__ float load(const float *p) { return __ldg(p); }
+    static __device__ __forceinline__ float from_byte(unsigned char b) { return (float)b; }
+    static __device__ __forceinline__ float store(float v) { return v; }
+};
+
+/* convert_rows_vec (fk_stage.cuh) with the scaled conversion */
+template <int NP>
+__device__ __forceinline__ void convert_rows_vec_s(const uint32_t *__restrict__ rp0,
+                                                   const uint32_t *__restrict__ rp1,
+                                                   float4 *__restrict__ tp, int tstride4, int bsh,
+                                                   const bool (&pred)[kMaxPanels - 1])
+{
+#pragma unroll 1
+    for (int i0 = 0; i0 < kWR; i0 += 4) {
+        uint32_t lo[4][NP], hi[4][NP];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                lo[i][p] = rp0[(i0 + i) * (kPanelB / 4) + p * kPanelWords];
+                hi[i][p] = rp1[(i0 + i) * (kPanelB / 4) + p * kPanelWords];
+            }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const float4 v = bytes_to_float4_s(__funnelshift_r(lo[i][p], hi[i][p], bsh));
+                if (pred[p]) tp[(i0 + i) * tstride4 + 32 * p] = v;
+            }
+    }
+}
+
+/*
  * Horizontal task, one panel of taps: acc[j] += sum_k g[k] * in[j + 3k], j in [0, 24), for
  * one tile row.  `trow` is the shared address of the first input float of the warp's
  * columns for this panel (16-byte aligned), `wts` of the panel's first tap; nchunk chunks of
@@ -213,12 +286,12 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
      * tile width); pc: chunks of four taps per panel */
     constexpr int C = kC;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw panels][TMA barrier, 64 B][colmap][per-warp taps x 2][tile][ring] */
+    /* layout: [raw panels][TMA barrier, 64 B][colmap][per-warp taps x 3][tile][ring] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
     int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
     float *wts = reinterpret_cast<float *>(colmap + cmw);
-    float *tile = wts + kWarps * 2 * wts_floats;
+    float *tile = wts + kWarps * 3 * wts_floats;
     float *ring = tile + kTB * twp; /* [kRowF columns][ipitch], icap rows used */
     const uint32_t ring_s = smem_u32(ring), tile_s = smem_u32(tile);
 
@@ -247,7 +320,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const int L = (int)((q.z >> 8) & 0x1fffu);
         const int n = 4 * ((L + 3) >> 2) + 4;
         const float *taps = pd.taps + q.w;
-        float *dst = wts + (warp * 2 + slot) * wts_floats;
+        float *dst = wts + (warp * 3 + slot) * wts_floats;
         for (int i = lane; i < n; i += 32) {
             const int in_range = i < L;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
@@ -275,10 +348,19 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wslot ^= 1) {
         q_nn = load_item(idx + 2 * stride); /* descriptor prefetch, two items ahead */
         const bool have_next = idx + stride < n_items;
-        const float *w_cur = wts + (warp * 2 + wslot) * wts_floats;
+        const float *w_cur = wts + (warp * 3 + wslot) * wts_floats; /* taps, V pass */
+        const float *w_h = w_cur;                                    /* taps, H pass */
         /* this item's taps were requested one item ago by this warp */
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
+        if (sizeof(T) == 1) { /* scaled copy for the H pass (see bytes_to_float4_s) */
+            float *hb = wts + (warp * 3 + 2) * wts_floats;
+            const int L = (int)((q_cur.z >> 8) & 0x1fffu);
+            const int n = 4 * ((L + 3) >> 2) + 4;
+            for (int i = lane; i < n; i += 32) hb[i] = w_cur[i] * kTapScaleH;
+            w_h = hb;
+            __syncwarp();
+        }
         /* request the next item's: that buffer held the previous item's taps */
         if (have_next) fill_taps(q_nxt, wslot ^ 1);
 
@@ -356,10 +438,10 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                 const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
                                 const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
                                 switch (np) {
-                                case 1: convert_rows_vec<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                case 2: convert_rows_vec<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                case 3: convert_rows_vec<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                default: convert_rows_vec<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                case 1: convert_rows_vec_s<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                case 2: convert_rows_vec_s<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                case 3: convert_rows_vec_s<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
+                                default: convert_rows_vec_s<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
                                 }
                             } else { /* rows clamp at the top / bottom edge of the image */
                                 for (int i = 0; i < kWR; i++) {
@@ -370,7 +452,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                         if (pred[p]) {
                                             const uint32_t lo = rp[i0 + p * kPanelWords];
                                             const uint32_t hi = rp[i1 + p * kPanelWords];
-                                            tp[32 * p] = bytes_to_float4(__funnelshift_r(lo, hi, bsh));
+                                            tp[32 * p] = bytes_to_float4_s(__funnelshift_r(lo, hi, bsh));
                                         }
                                     }
                                     tp += twp / 4;
@@ -395,7 +477,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                 float *tp = tile + (warp * kWR + i) * twp;
                                 for (int j = lane; j < pwz; j += 32) {
                                     const int m = f0 + j < twz ? colmap[f0 + j] : -1;
-                                    tp[j] = m >= 0 ? (float)rp[m] : 0.0f;
+                                    tp[j] = m >= 0 ? cols_px<T>::from_byte(rp[m]) : 0.0f;
                                 }
                             }
                         }
@@ -412,7 +494,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         float v[kWR];
 #pragma unroll
                         for (int i = 0; i < kWR; i++)
-                            v[i] = m >= 0 ? fast_px<T>::load(grow[i] + m) : 0.0f;
+                            v[i] = m >= 0 ? cols_px<T>::load(grow[i] + m) : 0.0f;
 #pragma unroll
                         for (int i = 0; i < kWR; i++) tp[i * twp + j] = v[i];
                     }
@@ -427,7 +509,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns */
                 if (active && lane < nrows)
                     h_part(tile_s + 4u * (uint32_t)(lane * twp + kSegF * warp),
-                           smem_u32(w_cur) + 16u * (uint32_t)c0, nch, hacc);
+                           smem_u32(w_h) + 16u * (uint32_t)c0, nch, hacc);
                 if (pn == npan - 1 && active && lane < nrows) {
                     int rr = rbm + lane;
                     rr = rr >= icap ? rr - icap : rr;
@@ -464,7 +546,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + col;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
-                            if (gi * kRV + j < fh) *op = fast_px<T>::store(acc[j]);
+                            if (gi * kRV + j < fh) *op = cols_px<T>::store(acc[j]);
                             op += (size_t)W * C;
                         }
                     }
@@ -497,7 +579,7 @@ cols_layout cols_layout_for(int max_length, bool tma, int npan)
     l.ipitch = (l.icap & 7) == 4 ? l.icap : l.icap + 4; /* 4 (mod 8) floats */
     l.npanel = tma ? (15 + (kSub + 2 * r) * kC + 4 + kPanelB - 1) / kPanelB : 0;
     l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)l.cmw * sizeof(int) +
-             ((size_t)kWarps * 2 * l.wts_floats + (size_t)kTB * twp + (size_t)kRowF * l.ipitch) *
+             ((size_t)kWarps * 3 * l.wts_floats + (size_t)kTB * twp + (size_t)kRowF * l.ipitch) *
                  sizeof(float);
     return l;
 }
