@@ -20,10 +20,11 @@
  *            the 32 rows of a warp read conflict-free.  Results go to the warp's columns of
  *            the intermediate, which is stored TRANSPOSED (ring[column][row]): consecutive
  *            lanes write consecutive words.  [CTA barrier B: the tile may be overwritten]
- *   V pass   one task = one float column x 8 output rows, read from the transposed
- *            intermediate with one LDS.128 per four rows; the 24 columns x (groups of 8 rows
- *            that are complete) of the warp are dealt to its 32 lanes, 96 tasks = three full
- *            rounds in the steady state.  Column pitch 4 (mod 8) floats: conflict-free.
+ *   V pass   one task = one RGB pixel (three columns) x 8 output rows, read from the
+ *            transposed intermediate with one LDS.128 per column and four rows; the warp's
+ *            8 pixels x the groups of 8 rows completed by the block (4 in the steady state)
+ *            are exactly one round of its 32 lanes.  Column pitch 4 (mod 8) floats:
+ *            conflict-free.
  *
  * Because a warp consumes in the V pass only what it produced itself in the H pass, the
  * intermediate needs no synchronisation at all and no slack for pipelining: it is a ring of
@@ -137,7 +138,6 @@ __device__ __forceinline__ void convert_rows_vec_s(const uint32_t *__restrict__ 
  * columns for this panel (16-byte aligned), `wts` of the panel's first tap; nchunk chunks of
  * four taps.  Ring of four slots of 12 input values: a chunk reads slots p, p+1, p+2 and
  * refills slot p+3 -- dead since the previous chunk -- with the values the NEXT chunk needs.
- * Whole turns of the ring first, then the last one to three chunks.
  */
 __device__ __forceinline__ void h_part(uint32_t trow, uint32_t wts, int nchunk,
                                        float (&acc)[kSegF])
@@ -176,48 +176,53 @@ __device__ __forceinline__ void h_part(uint32_t trow, uint32_t wts, int nchunk,
                 acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
         }
     };
-    int c = 0;
-    for (; c + 4 <= nchunk; c += 4) {
+    /* one copy of the four ring phases, left after the last chunk: the kernel is bound by
+     * instruction fetch as soon as its loops outgrow the instruction cache */
+    for (int c = 0; c < nchunk; c += 4) {
         chunk(0);
+        if (c + 1 >= nchunk) break;
         chunk(1);
+        if (c + 2 >= nchunk) break;
         chunk(2);
+        if (c + 3 >= nchunk) break;
         chunk(3);
-    }
-    if (c < nchunk) {
-        chunk(0);
-        if (c + 1 < nchunk) {
-            chunk(1);
-            if (c + 2 < nchunk) chunk(2);
-        }
     }
 }
 
 /*
- * Vertical task on the transposed intermediate: acc[j] = sum_k g[k] * col[row0 + j + k],
- * j < 8.  `col` is the shared-memory address of row 0 of the column, a ring of `cap` rows;
- * row0 and cap are multiples of 4, so a quad of rows never straddles the wrap.  Four-slot
- * register ring of four rows each, one LDS.128 a chunk ahead of its use.  The chunk loop
- * runs whole turns of the ring (no exit inside the unrolled body) and then the last one
- * to three chunks; addresses are raw 32-bit shared addresses so that stepping and wrapping
- * cost three integer instructions per chunk.
+ * Vertical task on the transposed intermediate: acc[j][k] = sum_t g[t] * col_k[row0 + j + t],
+ * j < 8 output rows, k < 3 adjacent columns (one RGB pixel).  `col` is the shared-memory
+ * address of row 0 of the first column, `cpitch` the bytes between columns; a column is a
+ * ring of `cap` rows; row0 and cap are multiples of 4, so a quad of rows never straddles the
+ * wrap.  Four-slot register ring of four rows per column, one LDS.128 per column a chunk
+ * ahead of its use.  The four load addresses of a turn of the ring are plain offsets unless
+ * the ring wraps inside the turn.
  */
-__device__ __forceinline__ void v_task_col(uint32_t col, int row0, int cap, uint32_t wts,
-                                           int nchunk, float (&acc)[kRV])
+__device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row0, int cap,
+                                          uint32_t wts, int nchunk, float (&acc)[kRV][kC])
 {
-    float win[16];
+    float win[kC][16];
 #pragma unroll
-    for (int j = 0; j < kRV; j++) acc[j] = 0.0f;
+    for (int j = 0; j < kRV; j++)
+#pragma unroll
+        for (int k = 0; k < kC; k++) acc[j][k] = 0.0f;
     const uint32_t end = col + 4u * (uint32_t)cap;
+    auto step = [&](uint32_t x) {
+        x += 16;
+        return x == end ? col : x;
+    };
     uint32_t a = col + 4u * (uint32_t)row0;
 #pragma unroll
     for (int v = 0; v < 3; v++) {
-        const float4 x = lds128(a);
-        win[4 * v + 0] = x.x;
-        win[4 * v + 1] = x.y;
-        win[4 * v + 2] = x.z;
-        win[4 * v + 3] = x.w;
-        a += 16;
-        a = a == end ? col : a;
+#pragma unroll
+        for (int k = 0; k < kC; k++) {
+            const float4 x = lds128(a + k * cpitch);
+            win[k][4 * v + 0] = x.x;
+            win[k][4 * v + 1] = x.y;
+            win[k][4 * v + 2] = x.z;
+            win[k][4 * v + 3] = x.w;
+        }
+        a = step(a);
     }
     float4 g4 = lds128(wts);
     uint32_t wa = wts + 16;
@@ -226,24 +231,24 @@ __device__ __forceinline__ void v_task_col(uint32_t col, int row0, int cap, uint
         const float g[4] = {g4.x, g4.y, g4.z, g4.w};
         g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
         wa += 16;
-        const float4 x = lds128(la);
-        win[(4 * (p + 3) + 0) % 16] = x.x;
-        win[(4 * (p + 3) + 1) % 16] = x.y;
-        win[(4 * (p + 3) + 2) % 16] = x.z;
-        win[(4 * (p + 3) + 3) % 16] = x.w;
+#pragma unroll
+        for (int k = 0; k < kC; k++) {
+            const float4 x = lds128(la + k * cpitch);
+            win[k][(4 * (p + 3) + 0) % 16] = x.x;
+            win[k][(4 * (p + 3) + 1) % 16] = x.y;
+            win[k][(4 * (p + 3) + 2) % 16] = x.z;
+            win[k][(4 * (p + 3) + 3) % 16] = x.w;
+        }
 #pragma unroll
         for (int t = 0; t < 4; t++) {
 #pragma unroll
             for (int j = 0; j < kRV; j++)
-                acc[j] = fmaf(g[t], win[(4 * p + t + j) % 16], acc[j]);
+#pragma unroll
+                for (int k = 0; k < kC; k++)
+                    acc[j][k] = fmaf(g[t], win[k][(4 * p + t + j) % 16], acc[j][k]);
         }
     };
-    auto step = [&](uint32_t x) {
-        x += 16;
-        return x == end ? col : x;
-    };
-    int c = 0;
-    for (; c + 4 <= nchunk; c += 4) {
+    for (int c = 0; c < nchunk; c += 4) {
         /* the four load addresses of this turn: plain offsets unless the ring wraps in it */
         uint32_t a1 = a + 16, a2 = a + 32, a3 = a + 48, an = a + 64;
         if (an >= end) {
@@ -253,21 +258,13 @@ __device__ __forceinline__ void v_task_col(uint32_t col, int row0, int cap, uint
             an = step(a3);
         }
         chunk(0, a);
+        if (c + 1 >= nchunk) break;
         chunk(1, a1);
+        if (c + 2 >= nchunk) break;
         chunk(2, a2);
+        if (c + 3 >= nchunk) break;
         chunk(3, a3);
         a = an;
-    }
-    if (c < nchunk) {
-        chunk(0, a);
-        if (c + 1 < nchunk) {
-            a = step(a);
-            chunk(1, a);
-            if (c + 2 < nchunk) {
-                a = step(a);
-                chunk(2, a);
-            }
-        }
     }
 }
 
@@ -311,6 +308,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const int c0a = (g.xs_c * C) & ~15;
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
         mbar_expect_tx(bar, (uint32_t)(g.npanel * kPanelBytes));
+#pragma unroll 1
         for (int p = 0; p < g.npanel; p++)
             tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
     };
@@ -378,6 +376,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             /* clamp-to-edge by index.  TMA: tile column -> byte offset inside the box; plain
              * loads: tile column -> element offset inside the image row.  Everybody is past
              * the last barrier of the previous item, so nobody reads the old map any more. */
+#pragma unroll 1
             for (int j = tid; j < twz; j += kThreads) {
                 int m = -1;
                 if (j < tw) {
@@ -396,13 +395,16 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         }
 
         const int ngroups = (fh + kRV - 1) / kRV; /* groups of 8 output rows */
-        const int nblk = (th + kTB - 1) / kTB;
+        /* The first block of an item is cut short so that the 2r rows of lead are absorbed
+         * there: from then on every block of 32 rows completes exactly four groups of 8 output
+         * rows -- one full round of the warp's lanes in the V pass.  (It moves the partial
+         * block of a strip from its end to its start.) */
+        const int lead = (2 * r) & (kTB - 1);
+        const int n_first = lead == 0 || lead > th ? (th < kTB ? th : kTB) : lead;
         const int npan = (nchunk + pc - 1) / pc;  /* tap panels of this item */
         int vdone = 0; /* output groups rendered so far */
         int rbm = 0;   /* ring row of the first tile row of the block */
-        for (int b = 0; b < nblk; b++) {
-            const int rb = b * kTB;
-            const int nrows = th - rb < kTB ? th - rb : kTB;
+        for (int rb = 0, nrows = n_first; rb < th; rb += nrows, nrows = th - rb < kTB ? th - rb : kTB) {
             const int ys = y0 - r + rb;
             const bool mine = warp * kWR < nrows; /* this warp converts rows of this block */
             float hacc[kSegF];
@@ -414,6 +416,18 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 const int f0 = 4 * C * c0;                        /* first tile float of the panel */
                 const int pwz = C * (8 * g.nseg + 4 + 4 * nch);   /* floats the H tasks may touch */
                 const int pval = tw - f0 < pwz ? tw - f0 : pwz;   /* of which image data */
+                if (vec && rb == 0 && npan == 1) {
+                    /* the columns beyond the image data once per item, in all eight rows the
+                     * warp owns whether or not the (short) first block reaches them: shared
+                     * memory starts out as whatever the previous kernel left there */
+                    const int nw = (pval + 3) >> 2, nq = (pwz >> 2) - nw;
+#pragma unroll 1
+                    for (int i = lane; i < nq * kWR; i += 32) {
+                        const int row = i / nq, q = i - row * nq;
+                        reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[nw + q] =
+                            make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
                 if (TMA) {
                     if (pn == 0) {
                         mbar_wait(bar, phase);
@@ -422,48 +436,44 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                     if (mine) {
                         const int ys_c = fast_clamp(ys, 0, H - 1);
                         if (vec) {
+                            /* tile word wj = raw bytes [sk + 4 wj, +4): two aligned words and a
+                             * funnel shift.  One column of 32 words x the warp's 8 rows per
+                             * iteration: 16 loads in flight, then 8 independent conversions.
+                             * Rows clamp at the top / bottom edge of the image through their
+                             * offsets inside the box (lanes past the tile read other shared
+                             * memory of this CTA, harmlessly). */
                             const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
                             const int sk = g.skew + f0; /* raw byte of the panel's first float */
                             const int bsh = (sk & 3) * 8;
-                            const int w0 = lane + (sk >> 2), w1 = w0 + 1;
-                            const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
-                            const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
                             const int nw = (pval + 3) >> 2; /* quads with image data */
-                            const int np = (nw + 31) >> 5;
-                            bool pred[kMaxPanels - 1];
+                            int roff[kWR];
 #pragma unroll
-                            for (int p = 0; p < kMaxPanels - 1; p++) pred[p] = lane + 32 * p < nw;
-                            float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp) + lane;
-                            if (ys >= 0 && ys + kTB <= H) {
-                                const uint32_t *rp0 = raw32 + warp * kWR * (kPanelB / 4) + i0;
-                                const uint32_t *rp1 = raw32 + warp * kWR * (kPanelB / 4) + i1;
-                                switch (np) {
-                                case 1: convert_rows_vec_s<1>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                case 2: convert_rows_vec_s<2>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                case 3: convert_rows_vec_s<3>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                default: convert_rows_vec_s<4>(rp0, rp1, tp, twp / 4, bsh, pred); break;
-                                }
-                            } else { /* rows clamp at the top / bottom edge of the image */
+                            for (int i = 0; i < kWR; i++)
+                                roff[i] = (fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c) * (kPanelB / 4);
+                            float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp);
+#pragma unroll 1
+                            for (int wj = lane; wj < nw; wj += 32) {
+                                const int w0 = wj + (sk >> 2), w1 = w0 + 1;
+                                const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
+                                const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
+                                uint32_t lo[kWR], hi[kWR];
+#pragma unroll
                                 for (int i = 0; i < kWR; i++) {
-                                    const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
-                                    const uint32_t *rp = raw32 + rr * (kPanelB / 4);
-#pragma unroll
-                                    for (int p = 0; p < kMaxPanels - 1; p++) {
-                                        if (pred[p]) {
-                                            const uint32_t lo = rp[i0 + p * kPanelWords];
-                                            const uint32_t hi = rp[i1 + p * kPanelWords];
-                                            tp[32 * p] = bytes_to_float4_s(__funnelshift_r(lo, hi, bsh));
-                                        }
-                                    }
-                                    tp += twp / 4;
+                                    lo[i] = raw32[roff[i] + i0];
+                                    hi[i] = raw32[roff[i] + i1];
                                 }
+#pragma unroll
+                                for (int i = 0; i < kWR; i++)
+                                    tp[i * (twp / 4) + wj] =
+                                        bytes_to_float4_s(__funnelshift_r(lo[i], hi[i], bsh));
                             }
                             /* the vector converter writes whole quads of image data only; the
                              * columns beyond, which only padded taps and discarded outputs
-                             * touch, are zeroed -- once per item, or every time when panels
-                             * of different widths share the tile */
-                            if (b == 0 || npan > 1) {
+                             * touch, are zeroed -- once per item (above), or every time when
+                             * panels of different widths share the tile */
+                            if (npan > 1) {
                                 const int nq = (pwz >> 2) - nw;
+#pragma unroll 1
                                 for (int i = lane; i < nq * kWR; i += 32) {
                                     const int row = i / nq, q = i - row * nq;
                                     reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[nw + q] =
@@ -471,10 +481,12 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                 }
                             }
                         } else {
+#pragma unroll 1
                             for (int i = 0; i < kWR; i++) {
                                 const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
                                 const unsigned char *rp = raw + rr * kPanelB;
                                 float *tp = tile + (warp * kWR + i) * twp;
+#pragma unroll 1
                                 for (int j = lane; j < pwz; j += 32) {
                                     const int m = f0 + j < twz ? colmap[f0 + j] : -1;
                                     tp[j] = m >= 0 ? cols_px<T>::from_byte(rp[m]) : 0.0f;
@@ -501,10 +513,8 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
                 __syncthreads(); /* A: the tile holds the panel */
                 if (TMA && tid == 0 && pn == npan - 1) { /* the raw bytes are free */
-                    if (rb + kTB < th)
-                        issue(g, rb + kTB);
-                    else if (have_next)
-                        issue(decode_item<C>(q_nxt, W), 0);
+                    const bool more = rb + nrows < th; /* next block, else the next item's first */
+                    if (more || have_next) issue(decode_item<C>(more ? q_cur : q_nxt, W), more ? rb + nrows : 0);
                 }
                 /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns */
                 if (active && lane < nrows)
@@ -519,7 +529,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 }
                 __syncthreads(); /* B: the tile may be overwritten; also orders H before V */
             }
-            rbm += kTB;
+            rbm += nrows;
             while (rbm >= icap) rbm -= icap;
 
             /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over the output
@@ -532,21 +542,25 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 jend = jend < ngroups ? jend : ngroups;
             }
             if (active) {
-                const int ntask = (jend - vdone) * kSegF;
+                /* one task = one RGB pixel x 8 rows; the warp's 8 pixels x the groups released
+                 * by this block (4 in the steady state) = one full round of its 32 lanes */
+                const int npx = ncol / C;
+                const int ntask = (jend - vdone) * 8;
                 for (int t = lane; t < ntask; t += 32) {
-                    const int gq = t / kSegF;
-                    const int col = t - gq * kSegF;
-                    const int gi = vdone + gq;
-                    if (col < ncol) {
+                    const int gi = vdone + (t >> 3), px = t & 7;
+                    if (px < npx) {
                         int r0 = gi * kRV;
                         while (r0 >= icap) r0 -= icap;
-                        float acc[kRV];
-                        v_task_col(ring_s + 4u * (uint32_t)((kSegF * warp + col) * ipitch), r0, icap,
-                                   smem_u32(w_cur), nchunk, acc);
-                        T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + col;
+                        float acc[kRV][C];
+                        v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
+                                  4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, acc);
+                        T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
-                            if (gi * kRV + j < fh) *op = cols_px<T>::store(acc[j]);
+                            if (gi * kRV + j < fh) {
+#pragma unroll
+                                for (int k = 0; k < C; k++) op[k] = cols_px<T>::store(acc[j][k]);
+                            }
                             op += (size_t)W * C;
                         }
                     }
