@@ -286,6 +286,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     /* layout: [raw panels][TMA barrier, 64 B][colmap][per-warp taps x 3][tile][ring] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
+    int *next_slot = reinterpret_cast<int *>(bar + 2); /* [2] item indices drawn by thread 0 */
     int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
     float *wts = reinterpret_cast<float *>(colmap + cmw);
     float *tile = wts + kWarps * 3 * wts_floats;
@@ -297,6 +298,11 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     const int warp = tid >> 5, lane = tid & 31;
     const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
     const int n_items = pd.counters[klass];
+    /* Items are dealt dynamically: a CTA starts with items blockIdx and blockIdx + grid and
+     * draws every further one from the class's cursor (zeroed before the render launches)
+     * when it starts an item, two items ahead of its use, so the draw, its hand-over through
+     * shared memory and the descriptor load all hide behind an item's work. */
+    int *cursor = pd.counters + FK_NCLASS + klass;
     const int stride = (int)gridDim.x;
     const uint4 none = make_uint4(0u, 0u, 0u, 0u);
     auto load_item = [&](int i) {
@@ -328,9 +334,9 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    int idx = (int)blockIdx.x;
+    int idx = (int)blockIdx.x, idx_nxt = idx + stride;
     uint4 q_cur = load_item(idx);
-    uint4 q_nxt = load_item(idx + stride);
+    uint4 q_nxt = load_item(idx_nxt);
     if (TMA && tid == 0) mbar_init(bar, 1);
     /* rows of the intermediate a padded tap can reach before they have been produced must
      * hold finite values, so start from zeros */
@@ -343,9 +349,10 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     uint32_t phase = 0;
     int wslot = 0;
     uint4 q_nn = none;
-    for (; idx < n_items; idx += stride, q_cur = q_nxt, q_nxt = q_nn, wslot ^= 1) {
-        q_nn = load_item(idx + 2 * stride); /* descriptor prefetch, two items ahead */
-        const bool have_next = idx + stride < n_items;
+    int idx_nn = n_items, par = 0;
+    for (; idx < n_items; idx = idx_nxt, idx_nxt = idx_nn, q_cur = q_nxt, q_nxt = q_nn, wslot ^= 1, par ^= 1) {
+        if (tid == 0) next_slot[par] = 2 * stride + atomicAdd(cursor, 1); /* read after barrier A */
+        const bool have_next = idx_nxt < n_items;
         const float *w_cur = wts + (warp * 3 + wslot) * wts_floats; /* taps, V pass */
         const float *w_h = w_cur;                                    /* taps, H pass */
         /* this item's taps were requested one item ago by this warp */
@@ -512,6 +519,10 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                     }
                 }
                 __syncthreads(); /* A: the tile holds the panel */
+                if (rb == 0 && pn == 0) { /* the item after the next: index, then descriptor */
+                    idx_nn = next_slot[par];
+                    q_nn = load_item(idx_nn);
+                }
                 if (TMA && tid == 0 && pn == npan - 1) { /* the raw bytes are free */
                     const bool more = rb + nrows < th; /* next block, else the next item's first */
                     if (more || have_next) issue(decode_item<C>(more ? q_cur : q_nxt, W), more ? rb + nrows : 0);

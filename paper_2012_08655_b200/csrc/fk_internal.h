@@ -35,33 +35,37 @@ enum {
  */
 #define FK_RECT 32
 #define FK_STRIP_ROWS 128
-#define FK_NCLASS 5
-/* Classes 0..2 are rendered by the fast kernel, each launch with the shared-memory layout
- * of the class's longest filter: 3 resident CTAs per SM up to 23 taps, 2 up to 63, 1 up to
- * 127.  Class 3 (longer filters) goes to the generic kernel, class 4 holds the identity
- * fragments (L = 1), which are plain copies. */
+#define FK_NCLASS 6
+/* Classes 0..3 are rendered by the fast kernels, each launch with the shared-memory layout
+ * of the class's longest filter: 3 resident CTAs per SM up to 23 and up to 39 taps, 2 up to
+ * 63 and (with the taps walked in panels, fk_blur_cols.cu) up to 127.  Class 4 (longer
+ * filters) goes to the generic kernel, class 5 holds the identity fragments (L = 1), which
+ * are plain copies. */
 #define FK_CLASS_L0 23
-#define FK_CLASS_L1 63
-#define FK_CLASS_L2 127
-#define FK_CLASS_GENERIC 3
-#define FK_CLASS_COPY 4
+#define FK_CLASS_L1 39
+#define FK_CLASS_L2 63
+#define FK_CLASS_L3 127
+#define FK_CLASS_GENERIC 4
+#define FK_CLASS_COPY 5
 
 static __host__ __device__ __forceinline__ int fk_class_of(int L)
 {
     return L <= 1 ? FK_CLASS_COPY
          : L <= FK_CLASS_L0 ? 0
          : L <= FK_CLASS_L1 ? 1
-         : L <= FK_CLASS_L2 ? 2 : FK_CLASS_GENERIC;
+         : L <= FK_CLASS_L2 ? 2
+         : L <= FK_CLASS_L3 ? 3 : FK_CLASS_GENERIC;
 }
 /* longest / shortest filter a class can hold */
 static inline int fk_class_lmax(int k)
 {
-    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, 8191, 1};
+    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, FK_CLASS_L3, 8191, 1};
     return lmax[k];
 }
 static inline int fk_class_lmin(int k)
 {
-    static const int lmin[FK_NCLASS] = {3, FK_CLASS_L0 + 2, FK_CLASS_L1 + 2, FK_CLASS_L2 + 2, 1};
+    static const int lmin[FK_NCLASS] = {3, FK_CLASS_L0 + 2, FK_CLASS_L1 + 2, FK_CLASS_L2 + 2,
+                                        FK_CLASS_L3 + 2, 1};
     return lmin[k];
 }
 
