@@ -28,7 +28,7 @@
  *
  * Because a warp consumes in the V pass only what it produced itself in the H pass, the
  * intermediate needs no synchronisation at all and no slack for pipelining: it is a ring of
- * 2r + 40 rows per column.  The only CTA-wide synchronisation left are the two barriers
+ * 2r + 32 rows per column.  The only CTA-wide synchronisation left are the two barriers
  * around the shared tile, and between them every warp has exactly the same amount of work.
  * The next block's TMA is issued right after barrier A and lands under the H and V passes.
  *
@@ -600,7 +600,9 @@ cols_layout cols_layout_for(int max_length, bool tma, int npan)
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
     l.cmw = (kC * (8 * kWarps + 4 + 4 * nchunk) + 3) & ~3; /* column map: the full width */
-    l.icap = (2 * r + 40 + 3) & ~3; /* see the header: no slack needed */
+    /* the intermediate: the short first block of an item aligns the blocks so that the V pass
+     * has consumed everything older than 2r rows when the next 32 rows are written */
+    l.icap = (2 * r + kTB + 3) & ~3;
     l.ipitch = (l.icap & 7) == 4 ? l.icap : l.icap + 4; /* 4 (mod 8) floats */
     l.npanel = tma ? (15 + (kSub + 2 * r) * kC + 4 + kPanelB - 1) / kPanelB : 0;
     l.smem = (size_t)l.npanel * kPanelBytes + 64 + (size_t)l.cmw * sizeof(int) +
