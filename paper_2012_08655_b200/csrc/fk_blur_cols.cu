@@ -428,12 +428,9 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                      * warp owns whether or not the (short) first block reaches them: shared
                      * memory starts out as whatever the previous kernel left there */
                     const int nw = (pval + 3) >> 2, nq = (pwz >> 2) - nw;
+                    float4 *zp = reinterpret_cast<float4 *>(tile + (warp * kWR + (lane >> 2)) * twp) + nw;
 #pragma unroll 1
-                    for (int i = lane; i < nq * kWR; i += 32) {
-                        const int row = i / nq, q = i - row * nq;
-                        reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[nw + q] =
-                            make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                    for (int q = lane & 3; q < nq; q += 4) zp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
                 if (TMA) {
                     if (pn == 0) {
@@ -453,26 +450,40 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                             const int sk = g.skew + f0; /* raw byte of the panel's first float */
                             const int bsh = (sk & 3) * 8;
                             const int nw = (pval + 3) >> 2; /* quads with image data */
-                            int roff[kWR];
-#pragma unroll
-                            for (int i = 0; i < kWR; i++)
-                                roff[i] = (fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c) * (kPanelB / 4);
-                            float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp);
+                            const int w00 = lane + (sk >> 2), w01 = w00 + 1;
+                            /* 32 words further along the row = same place in the next panel */
+                            const uint32_t *rl = raw32 + warp * kWR * (kPanelB / 4) +
+                                                 (w00 >> 5) * kPanelWords + (w00 & 31);
+                            const uint32_t *rh = raw32 + warp * kWR * (kPanelB / 4) +
+                                                 (w01 >> 5) * kPanelWords + (w01 & 31);
+                            float4 *tp = reinterpret_cast<float4 *>(tile + warp * kWR * twp) + lane;
+                            if (ys >= 0 && ys + kTB <= H) {
 #pragma unroll 1
-                            for (int wj = lane; wj < nw; wj += 32) {
-                                const int w0 = wj + (sk >> 2), w1 = w0 + 1;
-                                const int i0 = (w0 >> 5) * kPanelWords + (w0 & 31);
-                                const int i1 = (w1 >> 5) * kPanelWords + (w1 & 31);
-                                uint32_t lo[kWR], hi[kWR];
+                                for (int wj = lane; wj < nw; wj += 32) {
+                                    uint32_t lo[kWR], hi[kWR];
 #pragma unroll
-                                for (int i = 0; i < kWR; i++) {
-                                    lo[i] = raw32[roff[i] + i0];
-                                    hi[i] = raw32[roff[i] + i1];
+                                    for (int i = 0; i < kWR; i++) {
+                                        lo[i] = rl[i * (kPanelB / 4)];
+                                        hi[i] = rh[i * (kPanelB / 4)];
+                                    }
+#pragma unroll
+                                    for (int i = 0; i < kWR; i++)
+                                        tp[i * (twp / 4)] =
+                                            bytes_to_float4_s(__funnelshift_r(lo[i], hi[i], bsh));
+                                    rl += kPanelWords;
+                                    rh += kPanelWords;
+                                    tp += 32;
                                 }
-#pragma unroll
-                                for (int i = 0; i < kWR; i++)
-                                    tp[i * (twp / 4) + wj] =
-                                        bytes_to_float4_s(__funnelshift_r(lo[i], hi[i], bsh));
+                            } else { /* rows clamp at the top / bottom edge of the image */
+#pragma unroll 1
+                                for (int i = 0; i < kWR; i++) {
+                                    const int ro = (fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c -
+                                                    warp * kWR) * (kPanelB / 4);
+#pragma unroll 1
+                                    for (int wj = lane, o = 0; wj < nw; wj += 32, o += kPanelWords)
+                                        tp[i * (twp / 4) + wj - lane] = bytes_to_float4_s(
+                                            __funnelshift_r(rl[ro + o], rh[ro + o], bsh));
+                                }
                             }
                             /* the vector converter writes whole quads of image data only; the
                              * columns beyond, which only padded taps and discarded outputs
@@ -480,12 +491,11 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                              * panels of different widths share the tile */
                             if (npan > 1) {
                                 const int nq = (pwz >> 2) - nw;
+                                float4 *zp =
+                                    reinterpret_cast<float4 *>(tile + (warp * kWR + (lane >> 2)) * twp) + nw;
 #pragma unroll 1
-                                for (int i = lane; i < nq * kWR; i += 32) {
-                                    const int row = i / nq, q = i - row * nq;
-                                    reinterpret_cast<float4 *>(tile + (warp * kWR + row) * twp)[nw + q] =
-                                        make_float4(0.f, 0.f, 0.f, 0.f);
-                                }
+                                for (int q = lane & 3; q < nq; q += 4)
+                                    zp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                             }
                         } else {
 #pragma unroll 1
