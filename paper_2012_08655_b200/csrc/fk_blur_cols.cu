@@ -274,7 +274,7 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
  * TMA = false: plain-load staging (float32 frames, or buffers TMA cannot describe).
  */
 template <typename T, bool TMA>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
              const T *__restrict__ in, T *__restrict__ out, int klass, int wts_floats, int twp,
              int npanel_max, int icap, int ipitch, int cmw, int pc)
@@ -308,14 +308,20 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     auto load_item = [&](int i) {
         return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
     };
-    /* One 32-row block of an item: the box origin is clamped into the image so that every
-     * clamped source row / column of the block lies inside the box. */
+    /* One 32-row block of an item.  Rows: the box origin is clamped into the image so that
+     * every clamped source row of the block lies inside the box.  Columns: the box starts at
+     * the 16-byte boundary at or below the tile's first byte even when that lies left of the
+     * image (TMA takes negative coordinates and fills what is outside with zeros), so tile
+     * float j is always raw byte skew + j; the columns outside the image are patched with the
+     * edge pixel after the conversion. */
     auto issue = [&](const item_geo &g, int rb) {
-        const int c0a = (g.xs_c * C) & ~15;
+        const int byte0 = (g.x0 - g.r) * C;
+        const int c0a = byte0 & ~15;
+        const int np = (byte0 - c0a + g.tw + 4 + kPanelB - 1) / kPanelB;
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
-        mbar_expect_tx(bar, (uint32_t)(g.npanel * kPanelBytes));
+        mbar_expect_tx(bar, (uint32_t)(np * kPanelBytes));
 #pragma unroll 1
-        for (int p = 0; p < g.npanel; p++)
+        for (int p = 0; p < np; p++)
             tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
     };
     /* Zero-padded taps of an item into one of THIS WARP's two tap buffers with cp.async
@@ -375,26 +381,23 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const size_t frame_off = (size_t)g.f * H * W * C;
         const T *src = in + frame_off;
         T *dst = out + frame_off;
-        const bool vec = TMA && g.xin; /* vector converter, no column map */
+        const bool vec = TMA; /* vector converter; plain-load staging goes through a column map */
+        const int skew = ((x0 - r) * C) & 15;                      /* tile float 0 = raw byte skew */
+        const int nl = r - x0 > 0 ? r - x0 : 0;                    /* tile pixels left of the image */
+        const int nr = x0 + fw + r - W > 0 ? x0 + fw + r - W : 0; /* ... and right of it */
         const int ncol = fw * C - kSegF * warp < kSegF ? fw * C - kSegF * warp : kSegF;
         const bool active = ncol > 0; /* this warp owns columns of this item */
 
-        if (!vec) {
-            /* clamp-to-edge by index.  TMA: tile column -> byte offset inside the box; plain
-             * loads: tile column -> element offset inside the image row.  Everybody is past
-             * the last barrier of the previous item, so nobody reads the old map any more. */
+        if (!TMA) {
+            /* clamp-to-edge by index: tile column -> element offset inside the image row.
+             * Everybody is past the last barrier of the previous item, so nobody reads the old
+             * map any more. */
 #pragma unroll 1
             for (int j = tid; j < twz; j += kThreads) {
                 int m = -1;
                 if (j < tw) {
                     const int px = j / C, c = j - px * C;
-                    const int xx = fast_clamp(x0 - r + px, 0, W - 1);
-                    if (TMA) {
-                        m = g.skew + (xx - g.xs_c) * C + c;
-                        m = (m >> 7) * kPanelBytes + (m & (kPanelB - 1));
-                    } else {
-                        m = xx * C + c;
-                    }
+                    m = fast_clamp(x0 - r + px, 0, W - 1) * C + c;
                 }
                 colmap[j] = m;
             }
@@ -447,7 +450,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                              * offsets inside the box (lanes past the tile read other shared
                              * memory of this CTA, harmlessly). */
                             const uint32_t *raw32 = reinterpret_cast<const uint32_t *>(raw);
-                            const int sk = g.skew + f0; /* raw byte of the panel's first float */
+                            const int sk = skew + f0; /* raw byte of the panel's first float */
                             const int bsh = (sk & 3) * 8;
                             const int nw = (pval + 3) >> 2; /* quads with image data */
                             const int w00 = lane + (sk >> 2), w01 = w00 + 1;
@@ -497,16 +500,27 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                 for (int q = lane & 3; q < nq; q += 4)
                                     zp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                             }
-                        } else {
+                            if (nl | nr) {
+                                /* clamp-to-edge in x (blockwise.py:147): the tile columns left
+                                 * and right of the image repeat the edge pixel, read from the
+                                 * raw bytes of the same row */
+                                __syncwarp();
+                                const int el = skew + nl * C;                /* raw byte of pixel 0 */
+                                const int er = skew + (W - 1 - x0 + r) * C;  /* ... of pixel W-1 */
 #pragma unroll 1
-                            for (int i = 0; i < kWR; i++) {
-                                const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
-                                const unsigned char *rp = raw + rr * kPanelB;
-                                float *tp = tile + (warp * kWR + i) * twp;
+                                for (int i = 0; i < kWR; i++) {
+                                    const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
+                                    const unsigned char *rp = raw + rr * kPanelB;
+                                    float *trow = tile + (warp * kWR + i) * twp - f0;
 #pragma unroll 1
-                                for (int j = lane; j < pwz; j += 32) {
-                                    const int m = f0 + j < twz ? colmap[f0 + j] : -1;
-                                    tp[j] = m >= 0 ? cols_px<T>::from_byte(rp[m]) : 0.0f;
+                                    for (int j = lane; j < (nl + nr) * C; j += 32) {
+                                        const bool left = j < nl * C;
+                                        const int jg = left ? j : tw - (nl + nr) * C + j;
+                                        const int m = (left ? el : er) + jg % C;
+                                        if (jg >= f0 && jg < f0 + pwz)
+                                            trow[jg] = cols_px<T>::from_byte(
+                                                rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))]);
+                                    }
                                 }
                             }
                         }
