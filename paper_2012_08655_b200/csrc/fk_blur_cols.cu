@@ -623,7 +623,7 @@ cols_layout cols_layout_for(int max_length, bool tma, int npan)
     int twp = (twz + 3) & ~3;
     if ((twp & 7) != 4) twp += 4; /* pitch = 4 (mod 8) floats */
     l.twp = twp;
-    l.cmw = (kC * (8 * kWarps + 4 + 4 * nchunk) + 3) & ~3; /* column map: the full width */
+    l.cmw = tma ? 0 : (kC * (8 * kWarps + 4 + 4 * nchunk) + 3) & ~3; /* column map: plain loads only */
     /* the intermediate: the short first block of an item aligns the blocks so that the V pass
      * has consumed everything older than 2r rows when the next 32 rows are written */
     l.icap = (2 * r + kTB + 3) & ~3;
