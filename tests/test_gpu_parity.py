@@ -422,7 +422,8 @@ def test_fast_and_generic_kernels_agree_bit_for_bit():
         p = fk.FoveationParams(fragment_size=F, strength=1.3)
         outs = {}
         try:
-            for variant in (1, 2):      # 1 = generic kernel, 2 = fast kernel without TMA
+            # 1 = generic kernel, 2 = fast kernels without TMA, 3 = row-partitioned fast kernel
+            for variant in (1, 2, 3):
                 eng.set_kernel_variant(variant)
                 outs[variant] = fk.foveate_batch(frames, fix, p).clone()
         finally:
@@ -430,6 +431,38 @@ def test_fast_and_generic_kernels_agree_bit_for_bit():
         b = fk.foveate_batch(frames, fix, p)   # auto: TMA staging where the buffer allows
         assert torch.equal(outs[1], b), (shape, F, dtype)
         assert torch.equal(outs[2], b), (shape, F, dtype)
+        assert torch.equal(outs[3], b), (shape, F, dtype)
+
+
+def test_column_kernel_every_class_panels_and_strips_vs_generic():
+    """1080p frames with fixations in a corner, on an edge and in the middle: every tap-count
+    class of fk_blur_cols is populated -- filters past 63 taps are walked in tap panels,
+    same-filter fragments are merged into strips up to 128 rows, tiles hang over all four
+    image borders -- and the result must equal the generic kernel's bit for bit (uint8 with
+    and without TMA, float32)."""
+    eng = fk.get_engine(0)
+    rng = np.random.default_rng(2024)
+    h, w = 1080, 1920
+    fix = np.asarray([[0.0, 0.0], [1919.0, 540.0], [960.0, 540.0], [1300.5, 1079.0]])
+    n = len(fix)
+    u8 = torch.from_numpy(rng.integers(0, 256, (n, h, w, 3), dtype=np.uint8)).cuda()
+    f32 = torch.from_numpy(rng.random((2, h, w, 3), dtype=np.float32)).cuda()
+    for frames, fx, p in ((u8, fix, fk.FoveationParams()),
+                          (f32, fix[:2], fk.FoveationParams(e2=1.5))):
+        outs = {}
+        try:
+            for variant in (1, 2):
+                eng.set_kernel_variant(variant)
+                outs[variant] = fk.foveate_batch(frames, fx, p).clone()
+        finally:
+            eng.set_kernel_variant(0)
+        got = fk.foveate_batch(frames, fx, p)
+        assert torch.equal(outs[1], got)
+        assert torch.equal(outs[2], got)
+    # the corner fixation reaches the 103-tap filter (class 3)
+    _, _, bank, stats = fk.foveate(fk.RasterImage.from_array(u8[0].cpu().numpy()),
+                                   fk.FoveationParams(fixation=(0.0, 0.0)))
+    assert stats.max_filter >= 101
 
 
 def test_tma_path_border_and_interior_tiles_vs_generic():
