@@ -19,7 +19,8 @@
  *            (h_task_acc, fk_stage.cuh).  The row pitch of the tile is 4 (mod 8) floats, so
  *            the 32 rows of a warp read conflict-free.  Results go to the warp's columns of
  *            the intermediate, which is stored TRANSPOSED (ring[column][row]): consecutive
- *            lanes write consecutive words.  [CTA barrier B: the tile may be overwritten]
+ *            lanes write consecutive words.  [split barrier B: a warp arrives here and waits
+ *            only before the next conversion, so the V pass absorbs the skew between warps]
  *   V pass   one task = one RGB pixel (three columns) x 8 output rows, read from the
  *            transposed intermediate with one LDS.128 per column and four rows; the warp's
  *            8 pixels x the groups of 8 rows completed by the block (4 in the steady state)
@@ -286,6 +287,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     /* layout: [raw panels][TMA barrier, 64 B][colmap][per-warp taps x 3][tile][ring] */
     unsigned char *raw = smem_raw;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (TMA ? npanel_max * kPanelBytes : 0));
+    uint64_t *hbar = bar + 1;                           /* "H pass done": one arrival per warp */
     int *next_slot = reinterpret_cast<int *>(bar + 2); /* [2] item indices drawn by thread 0 */
     int *colmap = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(bar) + 64);
     float *wts = reinterpret_cast<float *>(colmap + cmw);
@@ -343,7 +345,10 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     int idx = (int)blockIdx.x, idx_nxt = idx + stride;
     uint4 q_cur = load_item(idx);
     uint4 q_nxt = load_item(idx_nxt);
-    if (TMA && tid == 0) mbar_init(bar, 1);
+    if (tid == 0) {
+        if (TMA) mbar_init(bar, 1);
+        mbar_init(hbar, kWarps);
+    }
     /* rows of the intermediate a padded tap can reach before they have been produced must
      * hold finite values, so start from zeros */
     for (int i = tid; i < kRowF * ipitch / 4; i += kThreads)
@@ -352,7 +357,8 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     __syncthreads();
     if (TMA && tid == 0 && idx < n_items) issue(decode_item<C>(q_cur, W), 0);
 
-    uint32_t phase = 0;
+    uint32_t phase = 0, hphase = 0;
+    bool hpend = false; /* an "H pass done" phase has been arrived at and not yet waited for */
     int wslot = 0;
     uint4 q_nn = none;
     int idx_nn = n_items, par = 0;
@@ -426,6 +432,14 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                 const int f0 = 4 * C * c0;                        /* first tile float of the panel */
                 const int pwz = C * (8 * g.nseg + 4 + 4 * nch);   /* floats the H tasks may touch */
                 const int pval = tw - f0 < pwz ? tw - f0 : pwz;   /* of which image data */
+                /* The tile is free once every warp is through the previous H pass.  That
+                 * barrier is split: a warp arrives right after its H pass and waits only here,
+                 * so the V pass in between absorbs whatever skew the warps have. */
+                if (hpend) {
+                    mbar_wait(hbar, hphase);
+                    hphase ^= 1;
+                    hpend = false;
+                }
                 if (vec && rb == 0 && npan == 1) {
                     /* the columns beyond the image data once per item, in all eight rows the
                      * warp owns whether or not the (short) first block reaches them: shared
@@ -562,7 +576,9 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 #pragma unroll
                     for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
                 }
-                __syncthreads(); /* B: the tile may be overwritten; also orders H before V */
+                __syncwarp(); /* the warp's own rows of the intermediate, before its V pass */
+                if (lane == 0) mbar_arrive(hbar);
+                hpend = true;
             }
             rbm += nrows;
             while (rbm >= icap) rbm -= icap;
