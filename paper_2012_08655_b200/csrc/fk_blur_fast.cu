@@ -5,7 +5,7 @@
  * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
  * (convolve.py:15).  What differs from fk_blur_generic is only how the work is laid out:
  *
- *   work items  strips at most 32 pixels wide and 128 tall with one filter each (vertical
+ *   work items  strips at most 32 pixels wide and 256 tall with one filter each (vertical
  *               runs of same-filter fragments share the horizontal pass over the halo rows
  *               between them), taken from the plan's per-class lists (fk_internal.h) by
  *               persistent CTAs of 128 threads,
@@ -195,10 +195,10 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         const bool wide = (fw * C) % 4 == 0;
         int jdone = 0, rbm = rpos;                /* groups released; ring row of block start */
         int pend_b = 0, pend_e = 0;               /* groups released by the previous block */
-        auto ring_row = [&](int k) { /* ring position of this item's tile row k (k < 2 icap) */
+        auto ring_row = [&](int k) { /* ring position of this item's tile row k */
             int p = rpos + k;
-            p = p >= icap ? p - icap : p;
-            return p >= icap ? p - icap : p;
+            while (p >= icap) p -= icap;
+            return p;
         };
         /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over output groups
          * [jb, je): 8 output rows each, read from the ring */

@@ -34,7 +34,7 @@ enum {
  * fits its longest filter.  Inside a list, a frame's items are contiguous.
  */
 #define FK_RECT 32
-#define FK_STRIP_ROWS 128
+#define FK_STRIP_ROWS 256
 #define FK_NCLASS 6
 /* Classes 0..3 are rendered by the fast kernels, each launch with the shared-memory layout
  * of the class's longest filter: 3 resident CTAs per SM up to 23 and up to 39 taps, 2 up to

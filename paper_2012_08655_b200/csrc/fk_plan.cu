@@ -60,9 +60,9 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  * only on the image and its filter):
  *   across  m = FK_RECT / F neighbouring cells of a grid row (aligned groups after the
  *           leading partial cell) become one unit FK_RECT wide when they share their taps;
- *   down    vertically adjacent equal units (same cells, same taps) inside an aligned block
- *           of FK_STRIP_ROWS / F grid rows become one strip, which lets them share the
- *           horizontal pass over the 2r halo rows between them.
+ *   down    a vertical run of equal units (same cells, same taps) is cut from its top into
+ *           strips of at most FK_STRIP_ROWS / F grid rows, which lets the fragments of a
+ *           strip share the horizontal pass over the 2r halo rows between them.
  * Wider fragments are cut into columns FK_RECT wide (and pieces FK_STRIP_ROWS tall) without
  * merging across cells.
  */
@@ -116,10 +116,14 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
             unit_of(y, gx, a0, a1);
             return a0 == u0 && a1 == u1 && len[y * gw + gx] == L && off[y * gw + gx] == o;
         };
-        const int blk0 = (gy / maxc) * maxc; /* strips do not cross aligned blocks of rows */
-        if (gy > blk0 && same(gy - 1)) return 0;
+        /* a vertical run of equal units is cut greedily from its top into strips of at
+         * most maxc cells: this cell heads one iff its distance to the top of the run is a
+         * multiple of maxc */
+        int up = 0;
+        while (gy - up - 1 >= 0 && same(gy - up - 1)) up++;
+        if (up % maxc != 0) return 0;
         int n = 1;
-        while (gy + n < blk0 + maxc && gy + n < gh && same(gy + n)) n++;
+        while (n < maxc && gy + n < gh && same(gy + n)) n++;
         return n;
     };
     /* rectangle s of the strip headed by cell c; false when it is empty, which happens for
