@@ -270,6 +270,48 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
 }
 
 /*
+ * Rare paths of the converter, kept out of line so that neither their code nor the index
+ * arithmetic the compiler would hoist for them sits in the per-block path:
+ * rows that clamp at the top / bottom edge of the image (the warp's 8 rows, one at a time) ...
+ */
+__device__ __noinline__ void convert_rows_clamped(const uint32_t *rl, const uint32_t *rh,
+                                                  float4 *tp /* lane 0's */, int tstride4, int bsh, int nw,
+                                                  int lane, int row_first, int box_first, int H)
+{
+#pragma unroll 1
+    for (int i = 0; i < kWR; i++) {
+        /* offset of the clamped source row relative to the warp's first row inside the box */
+        const int ro = (fast_clamp(row_first + i, 0, H - 1) - box_first) * (kPanelB / 4);
+#pragma unroll 1
+        for (int wj = lane, o = 0; wj < nw; wj += 32, o += kPanelWords)
+            tp[i * tstride4 + wj] =
+                bytes_to_float4_s(__funnelshift_r(rl[ro + o], rh[ro + o], bsh));
+    }
+}
+/* ... and tile columns left / right of the image, which repeat the edge pixel (clamp-to-edge
+ * in x, blockwise.py:147), read from the raw bytes of the same row.  `trow0` is the warp's
+ * first tile row shifted by the panel's first float, el / er the raw bytes of pixel 0 / W-1. */
+__device__ __noinline__ void patch_x_edges(const unsigned char *raw, float *trow0, int twp,
+                                           int lane, int row_first, int box_first, int H, int nl,
+                                           int nr, int tw, int el, int er, int f0, int pwz)
+{
+#pragma unroll 1
+    for (int i = 0; i < kWR; i++) {
+        const unsigned char *rp = raw + (fast_clamp(row_first + i, 0, H - 1) - box_first) * kPanelB;
+        float *trow = trow0 + i * twp;
+#pragma unroll 1
+        for (int j = lane; j < (nl + nr) * kC; j += 32) {
+            const bool left = j < nl * kC;
+            const int jg = left ? j : tw - (nl + nr) * kC + j;
+            const int m = (left ? el : er) + jg % kC;
+            if (jg >= f0 && jg < f0 + pwz)
+                trow[jg] = __uint_as_float(
+                    (uint32_t)rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))] << 16);
+        }
+    }
+}
+
+/*
  * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
  *              (W*3, H, N) with 128 x 32 x 1 boxes.
  * TMA = false: plain-load staging (float32 frames, or buffers TMA cannot describe).
@@ -492,15 +534,8 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                     tp += 32;
                                 }
                             } else { /* rows clamp at the top / bottom edge of the image */
-#pragma unroll 1
-                                for (int i = 0; i < kWR; i++) {
-                                    const int ro = (fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c -
-                                                    warp * kWR) * (kPanelB / 4);
-#pragma unroll 1
-                                    for (int wj = lane, o = 0; wj < nw; wj += 32, o += kPanelWords)
-                                        tp[i * (twp / 4) + wj - lane] = bytes_to_float4_s(
-                                            __funnelshift_r(rl[ro + o], rh[ro + o], bsh));
-                                }
+                                convert_rows_clamped(rl, rh, tp - lane, twp / 4, bsh, nw, lane,
+                                                     ys + warp * kWR, ys_c + warp * kWR, H);
                             }
                             /* the vector converter writes whole quads of image data only; the
                              * columns beyond, which only padded taps and discarded outputs
@@ -515,27 +550,10 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                                     zp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                             }
                             if (nl | nr) {
-                                /* clamp-to-edge in x (blockwise.py:147): the tile columns left
-                                 * and right of the image repeat the edge pixel, read from the
-                                 * raw bytes of the same row */
                                 __syncwarp();
-                                const int el = skew + nl * C;                /* raw byte of pixel 0 */
-                                const int er = skew + (W - 1 - x0 + r) * C;  /* ... of pixel W-1 */
-#pragma unroll 1
-                                for (int i = 0; i < kWR; i++) {
-                                    const int rr = fast_clamp(ys + warp * kWR + i, 0, H - 1) - ys_c;
-                                    const unsigned char *rp = raw + rr * kPanelB;
-                                    float *trow = tile + (warp * kWR + i) * twp - f0;
-#pragma unroll 1
-                                    for (int j = lane; j < (nl + nr) * C; j += 32) {
-                                        const bool left = j < nl * C;
-                                        const int jg = left ? j : tw - (nl + nr) * C + j;
-                                        const int m = (left ? el : er) + jg % C;
-                                        if (jg >= f0 && jg < f0 + pwz)
-                                            trow[jg] = cols_px<T>::from_byte(
-                                                rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))]);
-                                    }
-                                }
+                                patch_x_edges(raw, tile + warp * kWR * twp - f0, twp, lane,
+                                              ys + warp * kWR, ys_c, H, nl, nr, tw, skew + nl * C,
+                                              skew + (W - 1 - x0 + r) * C, f0, pwz);
                             }
                         }
                     }
@@ -576,9 +594,13 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 #pragma unroll
                     for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
                 }
-                __syncwarp(); /* the warp's own rows of the intermediate, before its V pass */
-                if (lane == 0) mbar_arrive(hbar);
-                hpend = true;
+                if (pn < npan - 1) {
+                    __syncthreads(); /* B between panels: the next conversion follows at once */
+                } else {
+                    __syncwarp(); /* the warp's own rows of the intermediate, before its V pass */
+                    if (lane == 0) mbar_arrive(hbar);
+                    hpend = true;
+                }
             }
             rbm += nrows;
             while (rbm >= icap) rbm -= icap;
