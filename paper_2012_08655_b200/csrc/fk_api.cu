@@ -259,6 +259,7 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     if (e == cudaSuccess) e = cudaMalloc(&d.raw_length, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.length, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.offset, cells * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.strip, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.items, FK_NCLASS * d.items_cap * sizeof(fk_item));
     if (e == cudaSuccess) e = cudaMalloc(&d.counters, 2 * FK_NCLASS * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.meta, (size_t)max_frames * FK_META_WORDS * sizeof(int32_t));
@@ -280,6 +281,7 @@ int fk_plan_destroy(fk_plan *p)
     cudaFree(p->d.raw_length);
     cudaFree(p->d.length);
     cudaFree(p->d.offset);
+    cudaFree(p->d.strip);
     cudaFree(p->d.items);
     cudaFree(p->d.counters);
     cudaFree(p->d.meta);

@@ -312,6 +312,47 @@ __device__ __noinline__ void patch_x_edges(const unsigned char *raw, float *trow
 }
 
 /*
+ * float32 frames whose tile lies inside the image in x: the warp's 8 rows are staged with
+ * 128-bit loads.  Tile quad q = image floats [s0 + 4q, +4) of the row, s0 = 3 (x0 - r): the
+ * aligned quad at or below it and the next one, shifted by REM = s0 mod 4 floats (a
+ * compile-time choice of registers).  `g0` points at the aligned quad of tile quad 0 in image
+ * row 0, `row_first` is the warp's first source row (rows clamp in y), `last` the last aligned
+ * quad of an image row that may be read.
+ */
+template <int REM>
+__device__ __forceinline__ void stage_rows_f32(const float *__restrict__ g0, int row_first, int H,
+                                               int rowstride, int aq0, int last,
+                                               float *__restrict__ tp, int twp, int lane, int nw,
+                                               int nq_all)
+{
+#pragma unroll 1
+    for (int q = lane; q < nq_all; q += 32) {
+        const bool ok = q < nw;
+        const bool okb = REM != 0 && ok && aq0 + q + 1 <= last;
+#pragma unroll 1
+        for (int i0 = 0; i0 < kWR; i0 += 4) { /* four rows in flight */
+            float4 a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float4 *rp = reinterpret_cast<const float4 *>(
+                                       g0 + (size_t)fast_clamp(row_first + i0 + i, 0, H - 1) * rowstride) + q;
+                a[i] = ok ? __ldg(rp) : make_float4(0.f, 0.f, 0.f, 0.f);
+                b[i] = okb ? __ldg(rp + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                float4 v;
+                if (REM == 0) v = a[i];
+                if (REM == 1) v = make_float4(a[i].y, a[i].z, a[i].w, b[i].x);
+                if (REM == 2) v = make_float4(a[i].z, a[i].w, b[i].x, b[i].y);
+                if (REM == 3) v = make_float4(a[i].w, b[i].x, b[i].y, b[i].z);
+                reinterpret_cast<float4 *>(tp + (i0 + i) * twp)[q] = v;
+            }
+        }
+    }
+}
+
+/*
  * TMA = true : T is uint8_t and `tmap` describes the input batch as a 3-D byte tensor
  *              (W*3, H, N) with 128 x 32 x 1 boxes.
  * TMA = false: plain-load staging (float32 frames, or buffers TMA cannot describe).
@@ -320,7 +361,7 @@ template <typename T, bool TMA>
 __global__ void __launch_bounds__(kThreads, 3)
 fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
              const T *__restrict__ in, T *__restrict__ out, int klass, int wts_floats, int twp,
-             int npanel_max, int icap, int ipitch, int cmw, int pc)
+             int npanel_max, int icap, int ipitch, int cmw, int pc, int f32vec)
 {
     /* twp: pitch of the working tile (one panel wide); cmw: ints in the column map (full
      * tile width); pc: chunks of four taps per panel */
@@ -557,6 +598,19 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                             }
                         }
                     }
+                } else if (mine && sizeof(T) == 4 && f32vec && nl == 0 && nr == 0) {
+                    /* float32 frames, tile inside the image in x: 128-bit loads */
+                    const int s0 = (x0 - r) * C + f0; /* image float of the panel's first float */
+                    const float *g0 = reinterpret_cast<const float *>(src) + (s0 & ~3);
+                    float *tp = tile + warp * kWR * twp;
+                    const int nw = (pval + 3) >> 2, nq_all = pwz >> 2;
+                    const int aq0 = s0 >> 2, last = (W * C) / 4 - 1;
+                    switch (s0 & 3) {
+                    case 0: stage_rows_f32<0>(g0, ys + warp * kWR, H, W * C, aq0, last, tp, twp, lane, nw, nq_all); break;
+                    case 1: stage_rows_f32<1>(g0, ys + warp * kWR, H, W * C, aq0, last, tp, twp, lane, nw, nq_all); break;
+                    case 2: stage_rows_f32<2>(g0, ys + warp * kWR, H, W * C, aq0, last, tp, twp, lane, nw, nq_all); break;
+                    default: stage_rows_f32<3>(g0, ys + warp * kWR, H, W * C, aq0, last, tp, twp, lane, nw, nq_all); break;
+                    }
                 } else if (mine) {
                     /* plain loads, eight rows in flight per lane */
                     const T *grow[kWR];
@@ -703,8 +757,11 @@ cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaSuccess;
     const int grid = h->prop.multiProcessorCount * occ;
+    /* float32 frames can be staged with 128-bit loads when rows start on 16-byte boundaries */
+    const int f32vec = sizeof(T) == 4 && ((uintptr_t)in & 15) == 0 && (pd.width * kC) % 4 == 0 &&
+                       ((size_t)pd.height * pd.width * kC) % 4 == 0;
     kernel<<<grid, kThreads, l.smem, s>>>(map, pd, (const T *)in, (T *)out, klass, l.wts_floats,
-                                          l.twp, l.npanel, l.icap, l.ipitch, l.cmw, l.pc);
+                                          l.twp, l.npanel, l.icap, l.ipitch, l.cmw, l.pc, f32vec);
     *taken = true;
     return cudaGetLastError();
 }

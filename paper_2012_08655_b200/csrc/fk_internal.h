@@ -90,6 +90,8 @@ struct fk_plan_dev {
     int32_t *raw_length; /* [frames][cap] */
     int32_t *length;     /* [frames][cap], foveal cell forced to 1 */
     int32_t *offset;     /* [frames][cap], tap offset inside `taps` */
+    int32_t *strip;      /* [frames][cap], scratch of the plan kernel: grid rows of the strip a
+                            cell heads (0: the cell belongs to a strip headed further up) */
     int32_t *meta;       /* [frames][FK_META_WORDS] */
     const float *taps;   /* fp32 tap table the offsets index (canonical LUT or custom) */
 };

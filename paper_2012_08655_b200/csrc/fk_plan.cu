@@ -101,29 +101,46 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
         u0 = g0;
         u1 = g1;
     };
+    /* Vertical runs of equal units are cut greedily from their top into strips of at most maxc
+     * cells.  One thread per grid column walks its column once and records, for every cell,
+     * the number of grid rows of the strip it heads (0: headed further up). */
+    int32_t *strip = pd.strip + (size_t)f * pd.cap;
+    for (int gx = tid; gx < gw; gx += nt) {
+        int head = -1, hu0 = 0, hu1 = 0, hL = 0, ho = 0;
+        for (int gy = 0; gy < gh; gy++) {
+            const int c = gy * gw + gx;
+            int u0 = gx, u1 = gx + 1;
+            const int L = len[c], o = off[c];
+            const bool mergeable = merge && L != 1;
+            if (mergeable) unit_of(gy, gx, u0, u1);
+            if (gx != u0) { /* inside a unit headed by the cell to its left */
+                strip[c] = 0;
+                head = -1;
+                continue;
+            }
+            if (mergeable && head >= 0 && gy - head < maxc && u0 == hu0 && u1 == hu1 && L == hL &&
+                o == ho) {
+                strip[c] = 0;
+                strip[head * gw + gx] += 1;
+            } else {
+                strip[c] = 1;
+                head = mergeable ? gy : -1;
+                hu0 = u0;
+                hu1 = u1;
+                hL = L;
+                ho = o;
+            }
+        }
+    }
+    __syncthreads();
     /* Cell c heads a strip of n grid rows of the unit [u0, u1); n = 0 when the cell belongs
      * to a strip headed by another cell. */
     auto strip_of = [&](int c, int &u0, int &u1) {
         const int gy = c / gw, gx = c - gy * gw;
         u0 = gx;
         u1 = gx + 1;
-        if (!merge || len[c] == 1) return 1;
-        unit_of(gy, gx, u0, u1);
-        if (gx != u0) return 0;
-        const int L = len[c], o = off[c];
-        auto same = [&](int y) {
-            int a0, a1;
-            unit_of(y, gx, a0, a1);
-            return a0 == u0 && a1 == u1 && len[y * gw + gx] == L && off[y * gw + gx] == o;
-        };
-        /* a vertical run of equal units is cut greedily from its top into strips of at
-         * most maxc cells: this cell heads one iff its distance to the top of the run is a
-         * multiple of maxc */
-        int up = 0;
-        while (gy - up - 1 >= 0 && same(gy - up - 1)) up++;
-        if (up % maxc != 0) return 0;
-        int n = 1;
-        while (n < maxc && gy + n < gh && same(gy + n)) n++;
+        const int n = strip[c];
+        if (n > 0 && merge && len[c] != 1) unit_of(gy, gx, u0, u1);
         return n;
     };
     /* rectangle s of the strip headed by cell c; false when it is empty, which happens for
