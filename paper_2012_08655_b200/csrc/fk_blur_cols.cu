@@ -275,38 +275,63 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
  * rows that clamp at the top / bottom edge of the image (the warp's 8 rows, one at a time) ...
  */
 __device__ __noinline__ void convert_rows_clamped(const uint32_t *rl, const uint32_t *rh,
-                                                  float4 *tp /* lane 0's */, int tstride4, int bsh, int nw,
-                                                  int lane, int row_first, int box_first, int H)
+                                                  float4 *tp /* lane 0's */, int tstride4, int bsh,
+                                                  int nw, int lane, int row_first, int box_first,
+                                                  int H)
 {
 #pragma unroll 1
-    for (int i = 0; i < kWR; i++) {
-        /* offset of the clamped source row relative to the warp's first row inside the box */
-        const int ro = (fast_clamp(row_first + i, 0, H - 1) - box_first) * (kPanelB / 4);
+    for (int i0 = 0; i0 < kWR; i0 += 4) { /* four rows in flight */
+        int ro[4]; /* offsets of the clamped source rows relative to the warp's first box row */
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            ro[i] = (fast_clamp(row_first + i0 + i, 0, H - 1) - box_first) * (kPanelB / 4);
 #pragma unroll 1
-        for (int wj = lane, o = 0; wj < nw; wj += 32, o += kPanelWords)
-            tp[i * tstride4 + wj] =
-                bytes_to_float4_s(__funnelshift_r(rl[ro + o], rh[ro + o], bsh));
+        for (int wj = lane, o = 0; wj < nw; wj += 32, o += kPanelWords) {
+            uint32_t lo[4], hi[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                lo[i] = rl[ro[i] + o];
+                hi[i] = rh[ro[i] + o];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                tp[(i0 + i) * tstride4 + wj] = bytes_to_float4_s(__funnelshift_r(lo[i], hi[i], bsh));
+        }
     }
 }
 /* ... and tile columns left / right of the image, which repeat the edge pixel (clamp-to-edge
  * in x, blockwise.py:147), read from the raw bytes of the same row.  `trow0` is the warp's
- * first tile row shifted by the panel's first float, el / er the raw bytes of pixel 0 / W-1. */
+ * first tile row shifted by the panel's first float, el / er the raw bytes of pixel 0 / W-1.
+ * Both runs start on a pixel, so the channel of a lane's element advances by 32 mod 3 = 2 per
+ * step of its loop. */
 __device__ __noinline__ void patch_x_edges(const unsigned char *raw, float *trow0, int twp,
                                            int lane, int row_first, int box_first, int H, int nl,
                                            int nr, int tw, int el, int er, int f0, int pwz)
 {
+    auto raw_at = [](const unsigned char *rp, int m) {
+        return __uint_as_float((uint32_t)rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))] << 16);
+    };
+    const int c0 = lane % kC;
+    const int lo = f0, hi = f0 + pwz; /* tile floats this panel holds */
 #pragma unroll 1
     for (int i = 0; i < kWR; i++) {
         const unsigned char *rp = raw + (fast_clamp(row_first + i, 0, H - 1) - box_first) * kPanelB;
         float *trow = trow0 + i * twp;
 #pragma unroll 1
-        for (int j = lane; j < (nl + nr) * kC; j += 32) {
-            const bool left = j < nl * kC;
-            const int jg = left ? j : tw - (nl + nr) * kC + j;
-            const int m = (left ? el : er) + jg % kC;
-            if (jg >= f0 && jg < f0 + pwz)
-                trow[jg] = __uint_as_float(
-                    (uint32_t)rp[(m >> 7) * kPanelBytes + (m & (kPanelB - 1))] << 16);
+        for (int side = 0; side < 2; side++) {
+            const int n = (side ? nr : nl) * kC;
+            if (n == 0) continue;
+            const int e = side ? er : el;
+            const float v0 = raw_at(rp, e), v1 = raw_at(rp, e + 1), v2 = raw_at(rp, e + 2);
+            const int base = side ? tw - n : 0;
+            int c = c0;
+#pragma unroll 1
+            for (int j = lane; j < n; j += 32) {
+                const int jg = base + j;
+                if (jg >= lo && jg < hi) trow[jg] = c == 0 ? v0 : (c == 1 ? v1 : v2);
+                c += 2;
+                c = c >= kC ? c - kC : c;
+            }
         }
     }
 }
