@@ -662,14 +662,22 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                     const bool more = rb + nrows < th; /* next block, else the next item's first */
                     if (more || have_next) issue(decode_item<C>(more ? q_cur : q_nxt, W), more ? rb + nrows : 0);
                 }
-                /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns */
-                if (active && lane < nrows)
-                    h_part(tile_s + 4u * (uint32_t)(lane * twp + kSegF * warp),
+                /* horizontal pass (blockwise.py:151): lane = tile row, the warp's 24 columns.
+                 * The short first block of an item (at most 24 rows, more blocks to follow, so
+                 * no V pass reads these rows before the next CTA barrier) is packed instead:
+                 * four adjacent lanes take the four column sets of one row, and the warps
+                 * left without rows skip the pass. */
+                const bool packed = rb == 0 && nrows <= 24 && nrows < th;
+                const int hrow = packed ? tid >> 2 : lane;
+                const int hset = packed ? tid & 3 : warp;
+                const bool hdo = hrow < nrows && kSegF * hset < fw * C;
+                if (hdo)
+                    h_part(tile_s + 4u * (uint32_t)(hrow * twp + kSegF * hset),
                            smem_u32(w_h) + 16u * (uint32_t)c0, nch, hacc);
-                if (pn == npan - 1 && active && lane < nrows) {
-                    int rr = rbm + lane;
+                if (pn == npan - 1 && hdo) {
+                    int rr = rbm + hrow;
                     rr = rr >= icap ? rr - icap : rr;
-                    float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
+                    float *rp = ring + (size_t)(kSegF * hset) * ipitch + rr;
 #pragma unroll
                     for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
                 }
