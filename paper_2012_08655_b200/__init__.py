@@ -39,6 +39,7 @@ from .blockwise import (
 )
 from .density import ingest_density_map
 from .engine import Engine, get_engine, pinned_empty, shard_range
+from .streaming import FoveationStream
 
 __version__ = "0.1.0"
 
@@ -49,5 +50,5 @@ __all__ = [
     "cell_of", "fragment_spans", "span_midpoints",
     "BlurGrid", "RenderStats", "Tile", "build_blur_grid", "compute_fragment_shift", "foveate",
     "foveate_batch", "plan", "render",
-    "Engine", "get_engine", "pinned_empty", "shard_range",
+    "Engine", "get_engine", "pinned_empty", "shard_range", "FoveationStream",
 ]
