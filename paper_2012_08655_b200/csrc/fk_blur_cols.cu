@@ -16,7 +16,7 @@
  *            working tile.  [CTA barrier A: the tile is complete]
  *   H pass   lane = tile row.  One task = the warp's 24 columns of that row: 24 accumulators,
  *            the input window in a four-slot register ring refilled a chunk ahead
- *            (h_task_acc, fk_stage.cuh).  The row pitch of the tile is 4 (mod 8) floats, so
+ *            (h_part).  The row pitch of the tile is 4 (mod 8) floats, so
  *            the 32 rows of a warp read conflict-free.  Results go to the warp's columns of
  *            the intermediate, which is stored TRANSPOSED (ring[column][row]): consecutive
  *            lanes write consecutive words.  [split barrier B: a warp arrives here and waits
@@ -32,6 +32,9 @@
  * 2r + 32 rows per column.  The only CTA-wide synchronisation left are the two barriers
  * around the shared tile, and between them every warp has exactly the same amount of work.
  * The next block's TMA is issued right after barrier A and lands under the H and V passes.
+ * The first block of an item is cut to 2r mod 32 rows, which makes every later block complete
+ * exactly four groups of 8 output rows (a full V round); that short block's H pass is packed
+ * four lanes per row so that the warps left without rows skip it.
  *
  * Long filters: the working tile is what limits the CTAs per SM, so for the classes with
  * long filters the taps are walked in up to four PANELS of `pc` chunks.  Panel p needs only
