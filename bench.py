@@ -237,8 +237,10 @@ def run_gpu(args):
 
     global W, H, F
     W, H, F = args.width, args.height, args.fragment
-    explore = (W, H, F, args.dtype, args.e2) != (1920, 1080, 32, "u8", 2.3)
+    explore = (W, H, F, args.dtype, args.e2, args.variant) != (1920, 1080, 32, "u8", 2.3, 0)
     eng = fk.get_engine(local)
+    if args.variant:
+        eng.set_kernel_variant(args.variant)
     params = fk.FoveationParams(fragment_size=F, e2=args.e2)
     n = args.frames
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
@@ -395,6 +397,8 @@ def main():
     ap.add_argument("--fragment", type=int, default=32, help="exploration only")
     ap.add_argument("--dtype", default="u8", choices=["u8", "f32"], help="exploration only")
     ap.add_argument("--e2", type=float, default=2.3, help="exploration only (CSF fit)")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="exploration only: fk_set_kernel_variant (0 = default kernels)")
     ap.add_argument("--fix-host", action="store_true",
                     help="exploration only: pass fixations from host memory each step")
     args = ap.parse_args()

@@ -734,6 +734,333 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     }
 }
 
+/* =====================================================================================
+ * fk_blur_bytes -- uint8 RGB frames: the H pass reads the TMA bytes directly.
+ *
+ * No working tile, no conversion pass, no CTA barrier.  One 4-D TMA box per 32-row block,
+ * over the batch seen as (16 bytes, rows, 16-byte chunks of a row, frames), lands the block
+ * as raw[chunk][row][16 B]: consecutive rows are 16 bytes apart, so lane = row reads are
+ * spread over all banks.  A lane walks its row as a stream of aligned 32-bit words: per
+ * chunk of four taps three new words, a funnel shift each to undo the byte misalignment of
+ * the tile, and one PRMT per byte into the denormal-linear fp32 encoding (bytes_to_float4_s)
+ * -- all on the integer pipe, under the 96 FFMAs of the chunk.  The word addresses repeat
+ * every 12 words (three chunks of 16 bytes) up to a constant, so a lane keeps 12 address
+ * registers and bumps each after use.  Rows clamp in y by picking the box row; columns
+ * outside the image are patched in the raw bytes (edge items only, with a CTA barrier).
+ * Everything after the H pass (transposed intermediate, V pass, dealing of items, taps) is
+ * fk_blur_cols.  Synchronisation: `bar` (TMA bytes landed, all warps wait) and `hbar` ("H pass
+ * done", one arrival per warp; thread 0 waits for it before it issues the next block's TMA).
+ * ===================================================================================== */
+constexpr int kQB = 16;            /* bytes per chunk */
+constexpr int kQStride = kQB * kTB; /* bytes between chunks in shared memory: 512 */
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1, int c2, int c3)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+/*
+ * Horizontal task on raw bytes: acc[j] += sum_k g[k] * byte[b0 + j + 3k], j in [0, 24), for one
+ * row.  `row_s` is the shared address of the row inside chunk 0 of the block, b0 the byte of
+ * the row (from the start of chunk 0) that is input 0 of this task.
+ */
+__device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, int nchunk,
+                                        float (&acc)[kSegF])
+{
+    constexpr int C = kC, NW = 16 * C;
+    float win[NW];
+    uint32_t ad[12]; /* addresses of the next 12 words of the stream */
+    const int w0 = b0 >> 2;
+    const uint32_t bsh = (uint32_t)(b0 & 3) * 8u;
+#pragma unroll
+    for (int i = 0; i < 12; i++) {
+        const int w = w0 + i;
+        ad[i] = row_s + (uint32_t)((w >> 2) * kQStride + (w & 3) * 4);
+    }
+    auto next_word = [&](const int i) { /* word i (mod 12) of the stream, then step its address */
+        const uint32_t v = lds32(ad[i]);
+        ad[i] += 3 * kQStride;
+        return v;
+    };
+    auto put = [&](const int slot4, uint32_t lo, uint32_t hi) { /* four floats from one shifted word */
+        const float4 f = bytes_to_float4_s(__funnelshift_r(lo, hi, bsh));
+        win[slot4 + 0] = f.x;
+        win[slot4 + 1] = f.y;
+        win[slot4 + 2] = f.z;
+        win[slot4 + 3] = f.w;
+    };
+    /* words 0..9: inputs 0..35 (slots 0..2); word 9 is carried as the low half of the next */
+    uint32_t carry = next_word(0);
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+        const uint32_t nx = next_word(k + 1);
+        put(4 * k, carry, nx);
+        carry = nx;
+    }
+    /* words 10, 11, 0 (of the next turn): loaded a chunk ahead of their conversion */
+    uint32_t n0 = next_word(10), n1 = next_word(11), n2 = next_word(0);
+    float4 g4 = lds128(wts);
+    uint32_t wa = wts + 16;
+    auto chunk = [&](const int p) {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
+        wa += 16;
+        /* slot p+3 <- the three words loaded during the previous chunk */
+        const int q = ((p + 3) % 4) * 4 * C;
+        put(q + 0, carry, n0);
+        put(q + 4, n0, n1);
+        put(q + 8, n1, n2);
+        carry = n2;
+        /* the next three words: stream indices 13 + 3c .. 15 + 3c = (1 + 3p) .. (3 + 3p) mod 12 */
+        n0 = next_word((1 + 3 * p) % 12);
+        n1 = next_word((2 + 3 * p) % 12);
+        n2 = next_word((3 + 3 * p) % 12);
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+#pragma unroll
+            for (int j = 0; j < kSegF; j++)
+                acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
+        }
+    };
+    for (int c = 0; c < nchunk; c += 4) {
+        chunk(0);
+        if (c + 1 >= nchunk) break;
+        chunk(1);
+        if (c + 2 >= nchunk) break;
+        chunk(2);
+        if (c + 3 >= nchunk) break;
+        chunk(3);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t *__restrict__ out,
+              int klass, int wts_floats, int nq, int icap, int ipitch)
+{
+    constexpr int C = kC;
+    typedef uint8_t T;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    /* layout: [raw: nq chunks x 32 rows x 16 B][barriers + item slots, 128 B][per-warp taps x 3][ring] */
+    unsigned char *raw = smem_raw;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + nq * kQStride);
+    uint64_t *hbar = bar + 1;
+    int *slot_idx = reinterpret_cast<int *>(bar + 2);                 /* [2] */
+    uint4 *slot_desc = reinterpret_cast<uint4 *>(bar + 4);            /* [2], 16-byte aligned */
+    float *wts = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(bar) + 128);
+    float *ring = wts + kWarps * 3 * wts_floats;
+    const uint32_t ring_s = smem_u32(ring), raw_s = smem_u32(raw);
+
+    const int W = pd.width, H = pd.height;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
+    const int n_items = pd.counters[klass];
+    int *cursor = pd.counters + FK_NCLASS + klass;
+    const int stride = (int)gridDim.x;
+    const uint4 none = make_uint4(0u, 0u, 0u, 0u);
+    auto load_item = [&](int i) {
+        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
+    };
+    /* One 32-row block: the box starts at the 16-byte chunk that holds the tile's first byte
+     * (possibly left of the image: TMA fills what is outside with zeros) and at the first
+     * source row clamped into the image. */
+    auto issue = [&](const uint4 q, int rb) {
+        const item_geo g = decode_item<C>(q, W);
+        const int byte0 = (g.x0 - g.r) * C;
+        const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
+        mbar_expect_tx(bar, (uint32_t)(nq * kQStride));
+        tma_load_4d(raw, &tmap, bar, 0, ys_c, byte0 >> 4, g.f);
+    };
+    auto fill_taps = [&](const uint4 q, int slot) {
+        const int L = (int)((q.z >> 8) & 0x1fffu);
+        const int n = 4 * ((L + 3) >> 2) + 4;
+        const float *taps = pd.taps + q.w;
+        float *dst = wts + (warp * 3 + slot) * wts_floats;
+        for (int i = lane; i < n; i += 32) {
+            const int in_range = i < L;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
+                         "l"(taps + (in_range ? i : 0)), "r"(in_range ? 4 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    /* Items: the first two are blockIdx and blockIdx + grid; every further one is drawn by
+     * thread 0 from the class's cursor when it starts an item, published (index and
+     * descriptor) in shared memory before its next TMA issue, and picked up by everybody
+     * after the first "bytes landed" wait of the following item. */
+    int idx = (int)blockIdx.x, idx_nxt = idx + stride;
+    uint4 q_cur = load_item(idx);
+    uint4 q_nxt = load_item(idx_nxt);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(hbar, kWarps);
+    }
+    for (int i = tid; i < kRowF * ipitch / 4; i += kThreads)
+        reinterpret_cast<float4 *>(ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (idx < n_items) fill_taps(q_cur, 0);
+    __syncthreads();
+    if (tid == 0 && idx < n_items) issue(q_cur, 0);
+
+    uint32_t phase = 0, hphase = 0;
+    int wslot = 0, par = 0, item_no = 0;
+    for (; idx < n_items; idx = idx_nxt, q_cur = q_nxt, wslot ^= 1, par ^= 1, item_no++) {
+        /* thread 0: draw the item after the next and start fetching its descriptor */
+        int d_idx = n_items;
+        uint4 d_q = none;
+        bool d_pending = false;
+        if (tid == 0) {
+            d_idx = 2 * stride + atomicAdd(cursor, 1);
+            d_q = load_item(d_idx);
+            d_pending = true;
+        }
+        const float *w_cur = wts + (warp * 3 + wslot) * wts_floats; /* taps, V pass */
+        float *w_h = wts + (warp * 3 + 2) * wts_floats;             /* scaled copy, H pass */
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        {
+            const int L = (int)((q_cur.z >> 8) & 0x1fffu);
+            const int n = 4 * ((L + 3) >> 2) + 4;
+            for (int i = lane; i < n; i += 32) w_h[i] = w_cur[i] * kTapScaleH;
+            __syncwarp();
+        }
+
+        const item_geo g = decode_item<C>(q_cur, W);
+        const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
+        const int nchunk = g.nchunk, th = g.th, tw = g.tw;
+        T *dst = out + (size_t)g.f * H * W * C;
+        const int skew = ((x0 - r) * C) & 15;                      /* tile float 0 = raw byte skew */
+        const int nl = r - x0 > 0 ? r - x0 : 0;                    /* tile pixels left of the image */
+        const int nr = x0 + fw + r - W > 0 ? x0 + fw + r - W : 0; /* ... and right of it */
+        const int ncol = fw * C - kSegF * warp < kSegF ? fw * C - kSegF * warp : kSegF;
+        const bool active = ncol > 0;
+        const int ngroups = (fh + kRV - 1) / kRV;
+        const int lead = (2 * r) & (kTB - 1);
+        const int n_first = lead == 0 || lead > th ? (th < kTB ? th : kTB) : lead;
+        int vdone = 0, rbm = 0;
+        bool have_next = idx_nxt < n_items;
+        for (int rb = 0, nrows = n_first; rb < th; rb += nrows, nrows = th - rb < kTB ? th - rb : kTB) {
+            const int ys = y0 - r + rb;
+            const int ys_c = fast_clamp(ys, 0, H - 1);
+            mbar_wait(bar, phase); /* the block's bytes have landed */
+            phase ^= 1;
+            if (rb == 0) {
+                if (item_no > 0) { /* the next item, published by thread 0 during the previous one */
+                    idx_nxt = slot_idx[par ^ 1];
+                    q_nxt = slot_desc[par ^ 1];
+                    have_next = idx_nxt < n_items;
+                }
+                if (have_next) fill_taps(q_nxt, wslot ^ 1);
+            }
+            if (nl | nr) {
+                /* clamp-to-edge in x (blockwise.py:147): overwrite the raw bytes left and right
+                 * of the image with the edge pixel, 8 box rows per warp */
+                const int el = skew + nl * C, er = skew + (W - 1 - x0 + r) * C;
+#pragma unroll 1
+                for (int i = 0; i < kWR; i++) {
+                    unsigned char *rowp = raw + (warp * kWR + i) * kQB;
+                    auto at = [&](int m) -> unsigned char & { return rowp[(m >> 4) * kQStride + (m & 15)]; };
+                    if (nl) {
+                        const unsigned char l0 = at(el), l1 = at(el + 1), l2 = at(el + 2);
+#pragma unroll 1
+                        for (int j = lane; j < nl * C; j += 32) {
+                            const int c = j % C;
+                            at(skew + j) = c == 0 ? l0 : (c == 1 ? l1 : l2);
+                        }
+                    }
+                    if (nr) {
+                        const unsigned char r0 = at(er), r1 = at(er + 1), r2 = at(er + 2);
+#pragma unroll 1
+                        for (int j = lane; j < nr * C; j += 32) {
+                            const int c = j % C;
+                            at(skew + tw - nr * C + j) = c == 0 ? r0 : (c == 1 ? r1 : r2);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            /* horizontal pass (blockwise.py:151): lane = tile row (clamped in y through the
+             * box row it reads), the warp's 24 columns */
+            if (active && lane < nrows) {
+                float hacc[kSegF];
+#pragma unroll
+                for (int j = 0; j < kSegF; j++) hacc[j] = 0.0f;
+                const int brow = fast_clamp(ys + lane, 0, H - 1) - ys_c; /* box row */
+                h_bytes(raw_s + (uint32_t)(brow * kQB), skew + kSegF * warp, smem_u32(w_h), nchunk,
+                        hacc);
+                int rr = rbm + lane;
+                rr = rr >= icap ? rr - icap : rr;
+                float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
+#pragma unroll
+                for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(hbar); /* this warp is through with the raw bytes */
+            if (warp == 0) {
+                /* every warp is through: publish the drawn item, then the next block's (or the
+                 * next item's first) bytes */
+                mbar_wait(hbar, hphase);
+                if (lane == 0) {
+                    if (d_pending) {
+                        slot_idx[par] = d_idx;
+                        slot_desc[par] = d_q;
+                        d_pending = false;
+                    }
+                    const bool more = rb + nrows < th;
+                    if (more || have_next) issue(more ? q_cur : q_nxt, more ? rb + nrows : 0);
+                }
+            }
+            hphase ^= 1;
+            rbm += nrows;
+            while (rbm >= icap) rbm -= icap;
+
+            /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) */
+            const int produced = rb + nrows;
+            int jend = ngroups;
+            if (produced < th) {
+                const int avail = produced - 2 * r - kRV;
+                jend = avail >= 0 ? avail / kRV + 1 : 0;
+                jend = jend < ngroups ? jend : ngroups;
+            }
+            if (active) {
+                const int npx = ncol / C;
+                const int ntask = (jend - vdone) * 8;
+                for (int t = lane; t < ntask; t += 32) {
+                    const int gi = vdone + (t >> 3), px = t & 7;
+                    if (px < npx) {
+                        int r0 = gi * kRV;
+                        while (r0 >= icap) r0 -= icap;
+                        float acc[kRV][C];
+                        v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
+                                  4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, acc);
+                        T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px;
+#pragma unroll
+                        for (int j = 0; j < kRV; j++) {
+                            if (gi * kRV + j < fh) {
+#pragma unroll
+                                for (int k = 0; k < C; k++) op[k] = cols_px<T>::store(acc[j][k]);
+                            }
+                            op += (size_t)W * C;
+                        }
+                    }
+                }
+            }
+            vdone = jend;
+        }
+    }
+}
+
 struct cols_layout {
     int wts_floats, twp, icap, ipitch, npanel, cmw, pc;
     size_t smem;
@@ -802,6 +1129,52 @@ cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     return cudaGetLastError();
 }
 
+/* The batch as (16 bytes, rows, 16-byte chunks of a row, frames) with boxes of
+ * 16 B x 32 rows x nq chunks: lands as [chunk][row][16 B] in shared memory. */
+bool make_tensor_map_chunks(CUtensorMap *map, const void *in, int W, int H, int n_frames, int nq)
+{
+    encode_tiled_fn enc = get_encode_tiled();
+    const size_t pitch = (size_t)W * kC;
+    if (!enc || ((uintptr_t)in & 15) != 0 || (pitch & 15) != 0 || nq > 256) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)kQB, (cuuint64_t)H, (cuuint64_t)(pitch / kQB), (cuuint64_t)n_frames};
+    cuuint64_t strides[3] = {(cuuint64_t)pitch, (cuuint64_t)kQB, (cuuint64_t)pitch * H};
+    cuuint32_t box[4] = {(cuuint32_t)kQB, (cuuint32_t)kTB, (cuuint32_t)nq, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(in), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+cudaError_t launch_bytes(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in, void *out,
+                         int n_frames, int class_length, cudaStream_t s, bool *taken)
+{
+    *taken = false;
+    const int nchunk = (class_length + 3) / 4;
+    const int r = (class_length - 1) / 2;
+    const int wts_floats = 4 * nchunk + 4;
+    const int nq = (168 + 6 * r + kQB - 1) / kQB; /* chunks a lane's word stream can reach */
+    const int icap = (2 * r + kTB + 3) & ~3;
+    const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
+    const size_t smem = (size_t)nq * kQStride + 128 +
+                        ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
+    if (smem > h->prop.sharedMemPerBlockOptin) return cudaSuccess;
+    CUtensorMap map;
+    memset(&map, 0, sizeof map);
+    if (!make_tensor_map_chunks(&map, in, pd.width, pd.height, n_frames, nq)) return cudaSuccess;
+    auto kernel = fk_blur_bytes;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaSuccess;
+    const int grid = h->prop.multiProcessorCount * occ;
+    kernel<<<grid, kThreads, smem, s>>>(map, pd, (uint8_t *)out, klass, wts_floats, nq, icap, ipitch);
+    *taken = true;
+    return cudaGetLastError();
+}
+
 } // namespace
 
 /* Renders the items of one class list of an RGB batch.  Returns cudaSuccess with
@@ -814,6 +1187,10 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
     CUtensorMap map;
     memset(&map, 0, sizeof map);
     if (is_f32) return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
+    if (h->variant == 5) { /* experiment: H pass straight from the TMA bytes */
+        cudaError_t e = launch_bytes(h, pd, klass, in, out, n_frames, class_length, s, taken);
+        if (e != cudaSuccess || *taken) return e;
+    }
     const bool tma = h->variant != 2 && make_tensor_map(&map, in, pd.width, pd.height, kC, n_frames);
     if (tma) return launch_cols<uint8_t, true>(h, map, pd, klass, in, out, class_length, s, taken);
     return launch_cols<uint8_t, false>(h, map, pd, klass, in, out, class_length, s, taken);
