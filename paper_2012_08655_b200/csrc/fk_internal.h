@@ -37,13 +37,14 @@ enum {
 #define FK_STRIP_ROWS 256
 #define FK_NCLASS 6
 /* Classes 0..3 are rendered by the fast kernels, each launch with the shared-memory layout
- * of the class's longest filter: 4 resident CTAs per SM up to 23 taps, 3 up to 47, 2 up to
- * 89 and (with the taps walked in panels, fk_blur_cols.cu) up to 127.  Class 4 (longer
- * filters) goes to the generic kernel, class 5 holds the identity fragments (L = 1), which
- * are plain copies. */
+ * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_cols for classes 0 and
+ * 1 (4 resident CTAs per SM up to 23 taps, 3 up to 47), fk_blur_bytes for classes 2 and 3
+ * (4 up to 67 taps, 3 up to 127).  Everything else: fk_blur_cols, with the taps walked in
+ * panels where its working tile would not fit twice on an SM.  Class 4 (longer filters)
+ * goes to the generic kernel, class 5 holds the identity fragments (L = 1), plain copies. */
 #define FK_CLASS_L0 23
 #define FK_CLASS_L1 47
-#define FK_CLASS_L2 89
+#define FK_CLASS_L2 67
 #define FK_CLASS_L3 127
 #define FK_CLASS_GENERIC 4
 #define FK_CLASS_COPY 5
