@@ -39,12 +39,13 @@ enum {
 /* Classes 0..3 are rendered by the fast kernels, each launch with the shared-memory layout
  * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_cols for classes 0 and
  * 1 (4 resident CTAs per SM up to 23 taps, 3 up to 47), fk_blur_bytes for classes 2 and 3
- * (4 up to 67 taps, 3 up to 127).  Everything else: fk_blur_cols, with the taps walked in
- * panels where its working tile would not fit twice on an SM.  Class 4 (longer filters)
+ * (3 CTAs per SM, up to 89 and up to 127 taps).  Everything else (float32 frames, buffers TMA
+ * cannot describe): fk_blur_cols, 2 CTAs per SM in class 2 with a whole-width working tile and
+ * in class 3 with the taps walked in panels.  Class 4 (longer filters)
  * goes to the generic kernel, class 5 holds the identity fragments (L = 1), plain copies. */
 #define FK_CLASS_L0 23
 #define FK_CLASS_L1 47
-#define FK_CLASS_L2 67
+#define FK_CLASS_L2 89
 #define FK_CLASS_L3 127
 #define FK_CLASS_GENERIC 4
 #define FK_CLASS_COPY 5
