@@ -208,8 +208,7 @@ cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream
 /*
  * Render every class list of a plan.  Classes whose shortest possible filter exceeds the
  * plan's bound are empty by construction and are not launched; longest filters first.
- * h->variant: 0 = fast kernels with generic fallback, 1 = generic kernel only,
- * 2 = fast kernels without TMA, 3 = row-partitioned fast kernel for RGB as well.
+ * h->variant: see fk_set_kernel_variant (include/fovea.h).
  */
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,

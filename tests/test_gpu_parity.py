@@ -422,21 +422,22 @@ def test_fast_and_generic_kernels_agree_bit_for_bit():
         p = fk.FoveationParams(fragment_size=F, strength=1.3)
         outs = {}
         try:
-            # 1 = generic kernel, 2 = fast kernels without TMA, 3 = row-partitioned fast kernel
-            for variant in (1, 2, 3):
+            # 1 = generic kernel, 2 = fast kernels without TMA, 3 = row-partitioned fast kernel,
+            # 4 = fk_blur_cols for every class, 5 = fk_blur_bytes for every class (include/fovea.h)
+            for variant in (1, 2, 3, 4, 5):
                 eng.set_kernel_variant(variant)
                 outs[variant] = fk.foveate_batch(frames, fix, p).clone()
         finally:
             eng.set_kernel_variant(0)
-        b = fk.foveate_batch(frames, fix, p)   # auto: TMA staging where the buffer allows
-        assert torch.equal(outs[1], b), (shape, F, dtype)
-        assert torch.equal(outs[2], b), (shape, F, dtype)
-        assert torch.equal(outs[3], b), (shape, F, dtype)
+        b = fk.foveate_batch(frames, fix, p)   # default dispatch
+        for variant in (1, 2, 3, 4, 5):
+            assert torch.equal(outs[variant], b), (shape, F, dtype, variant)
 
 
 def test_column_kernel_every_class_panels_and_strips_vs_generic():
     """1080p frames with fixations in a corner, on an edge and in the middle: every tap-count
-    class of fk_blur_cols is populated -- filters past 63 taps are walked in tap panels,
+    class of fk_blur_cols and fk_blur_bytes is populated -- filters past 89 taps are walked in
+    tap panels by fk_blur_cols,
     same-filter fragments are merged into strips up to 128 rows, tiles hang over all four
     image borders -- and the result must equal the generic kernel's bit for bit (uint8 with
     and without TMA, float32)."""
@@ -451,14 +452,14 @@ def test_column_kernel_every_class_panels_and_strips_vs_generic():
                           (f32, fix[:2], fk.FoveationParams(e2=1.5))):
         outs = {}
         try:
-            for variant in (1, 2):
+            for variant in (1, 2, 4, 5):
                 eng.set_kernel_variant(variant)
                 outs[variant] = fk.foveate_batch(frames, fx, p).clone()
         finally:
             eng.set_kernel_variant(0)
         got = fk.foveate_batch(frames, fx, p)
-        assert torch.equal(outs[1], got)
-        assert torch.equal(outs[2], got)
+        for variant in (1, 2, 4, 5):
+            assert torch.equal(outs[variant], got), variant
     # the corner fixation reaches the 103-tap filter (class 3)
     _, _, bank, stats = fk.foveate(fk.RasterImage.from_array(u8[0].cpu().numpy()),
                                    fk.FoveationParams(fixation=(0.0, 0.0)))
