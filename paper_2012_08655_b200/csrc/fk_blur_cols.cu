@@ -1016,6 +1016,9 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
                         slot_idx[par] = d_idx;
                         slot_desc[par] = d_q;
                         d_pending = false;
+                        __threadfence_block(); /* performed before the TMA request below: the
+                                                  other warps read the slot after they have
+                                                  seen bytes that request brought in */
                     }
                     const bool more = rb + nrows < th;
                     if (more || have_next) issue(more ? q_cur : q_nxt, more ? rb + nrows : 0);
