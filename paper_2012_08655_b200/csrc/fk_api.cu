@@ -106,6 +106,16 @@ int fk_create(int device, fk_handle **out)
             return rc;
         }
     }
+    for (int i = 0; i < fk_handle::kSide && e == cudaSuccess; i++) {
+        e = cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        int rc = fk_cuda_fail(nullptr, e, "side streams");
+        fk_destroy(h);
+        return rc;
+    }
     int rc = fk_build_lut(h, FK_LUT_DEFAULT_MAX, nullptr);
     if (rc != FK_OK) {
         g_err = h->err;
@@ -138,6 +148,11 @@ int fk_destroy(fk_handle *h)
     fk_release_stage(h);
     for (int i = 0; i < fk_handle::kStreams; i++)
         if (h->streams[i]) cudaStreamDestroy(h->streams[i]);
+    for (int i = 0; i < fk_handle::kSide; i++) {
+        if (h->side[i]) cudaStreamDestroy(h->side[i]);
+        if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+    }
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->lut64) cudaFree(h->lut64);
     if (h->lut32) cudaFree(h->lut32);
     if (h->probe) cudaFree(h->probe);
@@ -572,8 +587,9 @@ int fk_render_f32(fk_handle *h, const fk_plan *p, const float *in_dev, float *ou
 int fk_set_kernel_variant(fk_handle *h, int variant)
 {
     if (!h) return 0;
-    int old = h->variant;
-    h->variant = variant;
+    int old = h->variant | (h->serial_classes ? 16 : 0);
+    h->variant = variant & 15;
+    h->serial_classes = (variant & 16) != 0;
     return old;
 }
 

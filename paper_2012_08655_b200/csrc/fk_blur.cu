@@ -212,14 +212,33 @@ cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream
  */
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,
-                           cudaStream_t s, int *launches)
+                           cudaStream_t s0, int *launches)
 {
     /* rewind the render cursors (the counts stay) */
-    cudaError_t e = cudaMemsetAsync(pd.counters + FK_NCLASS, 0, FK_NCLASS * sizeof(int32_t), s);
+    cudaError_t e = cudaMemsetAsync(pd.counters + FK_NCLASS, 0, FK_NCLASS * sizeof(int32_t), s0);
     if (e != cudaSuccess) return e;
+    /* The class lists cover disjoint pixels and share nothing but read-only data, so every
+     * launch after the first goes to a side stream forked from s0 here and joined back below:
+     * the persistent CTAs of a class start on whatever SMs the previous class's last items
+     * leave idle instead of waiting for its tail. */
+    const bool fork = !h->serial_classes;
+    int nside = 0;
+    bool first = true;
+    /* the fork point precedes the first launch on s0, or the side streams would wait for it */
+    if (fork) {
+        e = cudaEventRecord(h->ev_fork, s0);
+        if (e != cudaSuccess) return e;
+    }
     for (int k = FK_CLASS_GENERIC; k >= 0; k--) {
         if (fk_class_lmin(k) > bound_length) continue;
         const int class_length = fk_class_lmax(k) < bound_length ? fk_class_lmax(k) : bound_length;
+        cudaStream_t s = s0;
+        if (fork && !first) {
+            s = h->side[nside++];
+            e = cudaStreamWaitEvent(s, h->ev_fork, 0);
+            if (e != cudaSuccess) return e;
+        }
+        first = false;
         bool taken = false;
         if (h->variant != 1 && k < FK_CLASS_GENERIC) {
             /* RGB: column-partitioned kernel; gray (and variant 3): row-partitioned kernel */
@@ -244,9 +263,14 @@ cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, 
     /* identity fragments */
     const int grid = h->prop.multiProcessorCount * 4;
     if (is_f32)
-        fk_copy_items<float><<<grid, 256, 0, s>>>(pd, (const float *)in, (float *)out, channels);
+        fk_copy_items<float><<<grid, 256, 0, s0>>>(pd, (const float *)in, (float *)out, channels);
     else
-        fk_copy_items<uint8_t><<<grid, 256, 0, s>>>(pd, (const uint8_t *)in, (uint8_t *)out, channels);
+        fk_copy_items<uint8_t><<<grid, 256, 0, s0>>>(pd, (const uint8_t *)in, (uint8_t *)out, channels);
     *launches += 1;
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    for (int i = 0; i < nside && e == cudaSuccess; i++) { /* join */
+        e = cudaEventRecord(h->ev_done[i], h->side[i]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, h->ev_done[i], 0);
+    }
+    return e;
 }

@@ -115,6 +115,14 @@ struct fk_handle {
     float *lut32 = nullptr;
     int variant = 0;
     int64_t launches = 0;
+    /* the class launches of one render run side by side: the class lists cover disjoint
+     * pixels, so the CTAs of the next class fill the SMs the previous one's tail leaves idle
+     * (fk_launch_blur forks from the caller's stream and joins back into it) */
+    static const int kSide = FK_NCLASS - 1;
+    cudaStream_t side[kSide] = {};
+    cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_done[kSide] = {};
+    int serial_classes = 0; /* fk_set_kernel_variant(v | 16): all classes on the caller's stream */
     /* pipeline resources of fk_foveate_host_* */
     static const int kStreams = 3;
     cudaStream_t streams[kStreams] = {nullptr, nullptr, nullptr};
