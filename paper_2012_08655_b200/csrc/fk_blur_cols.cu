@@ -1190,9 +1190,9 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
     CUtensorMap map;
     memset(&map, 0, sizeof map);
     if (is_f32) return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
-    /* uint8 by TMA: the classes with long filters (2 and 3) run the kernel whose H pass reads the
-     * TMA bytes directly -- no working tile, so 3 CTAs per SM where fk_blur_cols has 2; the
-     * short-filter classes are faster with the converted tile.  Variant 4: fk_blur_cols
+    /* uint8 by TMA: the classes with long filters (2 and up) run the kernel whose H pass reads
+     * the TMA bytes directly -- no working tile, so 4 or 3 CTAs per SM where fk_blur_cols has 2;
+     * the short-filter classes are a little faster with the converted tile.  Variant 4: fk_blur_cols
      * everywhere, variant 5: fk_blur_bytes everywhere. */
     if (h->variant == 5 || (h->variant == 0 && klass >= 2)) {
         cudaError_t e = launch_bytes(h, pd, klass, in, out, n_frames, class_length, s, taken);

@@ -35,20 +35,22 @@ enum {
  */
 #define FK_RECT 32
 #define FK_STRIP_ROWS 256
-#define FK_NCLASS 6
-/* Classes 0..3 are rendered by the fast kernels, each launch with the shared-memory layout
+#define FK_NCLASS 7
+/* Classes 0..4 are rendered by the fast kernels, each launch with the shared-memory layout
  * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_cols for classes 0 and
- * 1 (4 resident CTAs per SM up to 23 taps, 3 up to 47), fk_blur_bytes for classes 2 and 3
- * (3 CTAs per SM, up to 89 and up to 127 taps).  Everything else (float32 frames, buffers TMA
- * cannot describe): fk_blur_cols, 2 CTAs per SM in class 2 with a whole-width working tile and
- * in class 3 with the taps walked in panels.  Class 4 (longer filters)
- * goes to the generic kernel, class 5 holds the identity fragments (L = 1), plain copies. */
+ * 1 (4 resident CTAs per SM up to 23 taps, 3 up to 47), fk_blur_bytes for classes 2 to 4
+ * (4 CTAs per SM up to 69 taps, 3 up to 89 -- and up to 105 when the batch has nothing
+ * longer -- 2 up to 127).  Everything else (float32 frames, buffers TMA cannot describe):
+ * fk_blur_cols, 2 CTAs per SM in classes 2 and 3 with a whole-width working tile and in
+ * class 4 with the taps walked in panels.  Class 5 (longer filters) goes to the generic
+ * kernel, class 6 holds the identity fragments (L = 1), plain copies. */
 #define FK_CLASS_L0 23
 #define FK_CLASS_L1 47
-#define FK_CLASS_L2 89
-#define FK_CLASS_L3 127
-#define FK_CLASS_GENERIC 4
-#define FK_CLASS_COPY 5
+#define FK_CLASS_L2 69
+#define FK_CLASS_L3 89
+#define FK_CLASS_L4 127
+#define FK_CLASS_GENERIC 5
+#define FK_CLASS_COPY 6
 
 static __host__ __device__ __forceinline__ int fk_class_of(int L)
 {
@@ -56,18 +58,20 @@ static __host__ __device__ __forceinline__ int fk_class_of(int L)
          : L <= FK_CLASS_L0 ? 0
          : L <= FK_CLASS_L1 ? 1
          : L <= FK_CLASS_L2 ? 2
-         : L <= FK_CLASS_L3 ? 3 : FK_CLASS_GENERIC;
+         : L <= FK_CLASS_L3 ? 3
+         : L <= FK_CLASS_L4 ? 4 : FK_CLASS_GENERIC;
 }
 /* longest / shortest filter a class can hold */
 static inline int fk_class_lmax(int k)
 {
-    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, FK_CLASS_L3, 8191, 1};
+    static const int lmax[FK_NCLASS] = {FK_CLASS_L0, FK_CLASS_L1, FK_CLASS_L2, FK_CLASS_L3,
+                                        FK_CLASS_L4, 8191, 1};
     return lmax[k];
 }
 static inline int fk_class_lmin(int k)
 {
     static const int lmin[FK_NCLASS] = {3, FK_CLASS_L0 + 2, FK_CLASS_L1 + 2, FK_CLASS_L2 + 2,
-                                        FK_CLASS_L3 + 2, 1};
+                                        FK_CLASS_L3 + 2, FK_CLASS_L4 + 2, 1};
     return lmin[k];
 }
 
