@@ -186,6 +186,24 @@ int fk_host_free(void *ptr);
  * measured with CUDA events.  The roofline denominator when it is FP32-bound. */
 int fk_measure_fp32_peak(fk_handle *h, double *tflops, double *ms);
 
+/* ---- validation: SSIM map on the device ---------------------------------------------- */
+/* Replaces quality.ssim_map (quality.py:82-103): BT.601 luma of both images (quality.py:31-35),
+ * the five separable windowed means over fully-valid windows (quality.py:45-48) and the SSIM
+ * formula, fp64 throughout.  `ref_dev` / `test_dev`: device uint8 [height][width][channels],
+ * channels 1 or 3.  `window_host`: the window_size (<= 15) normalised taps, evaluated by the
+ * caller with the reference's expression (quality.py:38-42).  c1 = (K1 * range)^2,
+ * c2 = (K2 * range)^2.  `values_dev`: device float64 [height - window_size + 1][width -
+ * window_size + 1]; with accumulate != 0 the map is added onto what is there
+ * (mean_ssim_map, quality.py:106-114). */
+int fk_ssim_u8(fk_handle *h, const uint8_t *ref_dev, const uint8_t *test_dev, int width,
+               int height, int channels, const double *window_host, int window_size, double c1,
+               double c2, double *values_dev, int accumulate, void *stream);
+/* Replaces _map_from_values (quality.py:70-79): divides the `count` values by `divisor`
+ * in place (1.0: untouched), then stats_host[0..2] = mean, min, flat index of the first
+ * minimum (np.argmin).  Synchronises the stream. */
+int fk_ssim_stats(fk_handle *h, double *values_dev, int64_t count, double divisor,
+                  double *stats_host, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,12 +2,15 @@
 ``foveate`` path of foveakit (arXiv 2012.08655), backed by hand-written sm_100a CUDA
 kernels behind a C ABI (include/fovea.h, csrc/).
 
-Only the hot path is here: the reference's CLI, service, codecs,
-pyramid baseline and SSIM tooling are out of scope.  There is no CPU fallback: importing
-works anywhere, but every compute entry point needs a CUDA device.
+Only the hot path and its "next" rows are here: plan / render /
+foveate, density-map sigma fields, the latest-wins streaming layer, the timing harness, the
+command line for those (``python -m paper_2012_08655_b200``) and the SSIM checker
+(``quality``).  The reference's web service, pyramid baseline and per-pixel oracle are out of
+scope.  There is no CPU fallback: importing works anywhere, but every compute entry point
+needs a CUDA device.
 """
 
-from .imaging import RasterImage
+from .imaging import RasterImage, load_image, save_image
 from .retinal import (
     FoveationParams,
     SigmaField,
@@ -40,11 +43,13 @@ from .blockwise import (
 from .density import ingest_density_map
 from .engine import Engine, get_engine, pinned_empty, shard_range
 from .streaming import FoveationStream
+from .quality import SSIMMap, mean_ssim_map, ssim_map
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "RasterImage", "FoveationParams", "SigmaField", "build_sigma_field", "contrast_threshold",
+    "RasterImage", "load_image", "save_image", "SSIMMap", "ssim_map", "mean_ssim_map",
+    "FoveationParams", "SigmaField", "build_sigma_field", "contrast_threshold",
     "cutoff_cpd", "cutoff_cpp", "eccentricity_of", "ingest_density_map", "sigma_at",
     "FilterBank", "build_bank", "filter_length", "gaussian_filter_1d", "total_coefficients",
     "cell_of", "fragment_spans", "span_midpoints",

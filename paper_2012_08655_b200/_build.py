@@ -18,7 +18,7 @@ ROOT = PKG.parent
 LIB = CSRC / "libfovea.so"
 STAMP = CSRC / "libfovea.so.srchash"
 
-SOURCES = ["fk_api.cu", "fk_plan.cu", "fk_blur.cu", "fk_blur_fast.cu", "fk_blur_cols.cu"]
+SOURCES = ["fk_api.cu", "fk_plan.cu", "fk_blur.cu", "fk_blur_fast.cu", "fk_blur_cols.cu", "fk_ssim.cu"]
 HEADERS = ["fk_internal.h", "fk_hypot.h", "fk_stage.cuh", "../../include/fovea.h"]
 
 NVCC_FLAGS = [

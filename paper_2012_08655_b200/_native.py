@@ -22,7 +22,7 @@ EXPORTS = [
     "fk_plan_create", "fk_plan_destroy", "fk_plan_cell_capacity", "fk_plan_model",
     "fk_plan_density", "fk_plan_set_grid", "fk_plan_read", "fk_plan_read_lengths", "fk_render_u8",
     "fk_render_f32", "fk_set_kernel_variant", "fk_launch_count", "fk_foveate_host_u8",
-    "fk_foveate_host_f32", "fk_host_alloc", "fk_host_free", "fk_measure_fp32_peak",
+    "fk_foveate_host_f32", "fk_host_alloc", "fk_host_free", "fk_measure_fp32_peak", "fk_ssim_u8", "fk_ssim_stats",
 ]
 
 
@@ -87,6 +87,8 @@ def _declare(lib):
         "fk_host_alloc": (i32, [C.c_size_t, P(vp)]),
         "fk_host_free": (i32, [vp]),
         "fk_measure_fp32_peak": (i32, [vp, P(dbl), P(dbl)]),
+        "fk_ssim_u8": (i32, [vp, vp, vp, i32, i32, i32, vp, i32, dbl, dbl, vp, i32, vp]),
+        "fk_ssim_stats": (i32, [vp, vp, i64, dbl, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -156,6 +156,7 @@ int fk_destroy(fk_handle *h)
     if (h->lut64) cudaFree(h->lut64);
     if (h->lut32) cudaFree(h->lut32);
     if (h->probe) cudaFree(h->probe);
+    if (h->ssim_stats) cudaFree(h->ssim_stats);
     delete h;
     return FK_OK;
 }
@@ -714,6 +715,43 @@ int fk_measure_fp32_peak(fk_handle *h, double *tflops, double *ms_out)
     const double flops = 2.0 * 16.0 * (double)iters * (double)sm * 8.0 * 256.0;
     *tflops = flops / (best * 1e-3) / 1e12;
     if (ms_out) *ms_out = best;
+    return FK_OK;
+}
+
+/* ------------------------------------------------------------ SSIM (validation tool) */
+int fk_ssim_u8(fk_handle *h, const uint8_t *ref_dev, const uint8_t *test_dev, int width,
+               int height, int channels, const double *window_host, int window_size, double c1,
+               double c2, double *values_dev, int accumulate, void *stream)
+{
+    if (!h || !ref_dev || !test_dev || !window_host || !values_dev)
+        return fk_fail(h, FK_EINVAL, "NULL argument");
+    if (channels != 1 && channels != 3)
+        return fk_fail(h, FK_EINVAL, "channels must be 1 or 3, got %d", channels);
+    if (window_size < 1 || window_size > 15)
+        return fk_fail(h, FK_EINVAL, "window_size must be in [1, 15], got %d", window_size);
+    if (width < window_size || height < window_size) /* quality.py:88-89 */
+        return fk_fail(h, FK_EINVAL, "images must be at least %dpx per side", window_size);
+    FK_CUDA(h, cudaSetDevice(h->device));
+    FK_CUDA(h, fk_launch_ssim_map(ref_dev, test_dev, width, height, channels, window_host,
+                                  window_size, c1, c2, values_dev, accumulate, as_stream(stream)));
+    h->launches += 1;
+    return FK_OK;
+}
+
+int fk_ssim_stats(fk_handle *h, double *values_dev, int64_t count, double divisor,
+                  double *stats_host, void *stream)
+{
+    if (!h || !values_dev || !stats_host) return fk_fail(h, FK_EINVAL, "NULL argument");
+    if (count < 1) return fk_fail(h, FK_EINVAL, "empty map");
+    if (!(divisor > 0.0)) return fk_fail(h, FK_EINVAL, "divisor must be positive");
+    FK_CUDA(h, cudaSetDevice(h->device));
+    if (!h->ssim_stats) FK_CUDA(h, cudaMalloc(&h->ssim_stats, 3 * sizeof(double)));
+    cudaStream_t s = as_stream(stream);
+    FK_CUDA(h, fk_launch_ssim_stats(values_dev, (long long)count, divisor, h->ssim_stats, s));
+    h->launches += 1;
+    FK_CUDA(h, cudaMemcpyAsync(stats_host, h->ssim_stats, 3 * sizeof(double),
+                               cudaMemcpyDeviceToHost, s));
+    FK_CUDA(h, cudaStreamSynchronize(s));
     return FK_OK;
 }
 

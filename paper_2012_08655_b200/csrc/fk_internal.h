@@ -138,6 +138,7 @@ struct fk_handle {
     int stage_w = 0, stage_h = 0, stage_f = 0, stage_frames = 0;
     /* scratch for the FP32 peak probe */
     float *probe = nullptr;
+    double *ssim_stats = nullptr; /* [3] device scratch of fk_ssim_stats */
 };
 
 struct fk_plan {
@@ -178,6 +179,12 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
                                 void *out, int n_frames, int is_f32, int class_length,
                                 cudaStream_t s, bool *taken);
 cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s);
+/* fk_ssim.cu */
+cudaError_t fk_launch_ssim_map(const uint8_t *ref, const uint8_t *test, int W, int H, int C,
+                               const double *window, int n, double c1, double c2,
+                               double *values, int accumulate, cudaStream_t s);
+cudaError_t fk_launch_ssim_stats(double *values, long long count, double divisor,
+                                 double *stats_dev, cudaStream_t s);
 
 /* Host replica of the grid geometry (tiling.py:15-28). */
 static inline int fk_span_count(int extent, int F, int offset)

@@ -273,6 +273,40 @@ class Engine:
         return out
 
     # ---------------------------------------------------------------- measurement
+    # ----------------------------------------------------------------------- SSIM
+    def ssim_values(self, ref: torch.Tensor, test: torch.Tensor, window: np.ndarray, c1: float,
+                    c2: float, values=None, accumulate=False, stream=None) -> torch.Tensor:
+        """fk_ssim_u8: the SSIM map of two device images [H, W, C] as a float64 CUDA tensor
+        (optionally accumulated onto `values`)."""
+        for t in (ref, test):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8
+                    and t.ndim == 3 and t.is_contiguous() and t.device.index == self.device):
+                raise ValueError("ssim_values takes contiguous uint8 CUDA tensors [H, W, C]")
+        h, w, c = ref.shape
+        win = np.ascontiguousarray(window, dtype=np.float64)
+        n = int(win.shape[0])
+        if values is None:
+            if accumulate:
+                raise ValueError("accumulate needs a map to add onto")
+            values = torch.empty((max(h - n + 1, 1), max(w - n + 1, 1)), dtype=torch.float64,
+                                 device=ref.device)
+        with self._lock:
+            check(self._lib.fk_ssim_u8(self._h, C.c_void_p(ref.data_ptr()),
+                                       C.c_void_p(test.data_ptr()), int(w), int(h), int(c),
+                                       _np_ptr(win), n, float(c1), float(c2),
+                                       C.c_void_p(values.data_ptr()), int(bool(accumulate)),
+                                       self._stream(stream)), self._h)
+        return values
+
+    def ssim_stats(self, values: torch.Tensor, divisor: float = 1.0, stream=None):
+        """fk_ssim_stats: (mean, min, flat argmin) of a device map, after values /= divisor."""
+        out = np.empty(3, np.float64)
+        with self._lock:
+            check(self._lib.fk_ssim_stats(self._h, C.c_void_p(values.data_ptr()),
+                                          int(values.numel()), float(divisor), _np_ptr(out),
+                                          self._stream(stream)), self._h)
+        return float(out[0]), float(out[1]), int(out[2])
+
     def set_kernel_variant(self, variant: int) -> int:
         return int(self._lib.fk_set_kernel_variant(self._h, int(variant)))
 

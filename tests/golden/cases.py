@@ -83,3 +83,30 @@ DENSITY_RENDER_CASES = [
 
 def density_map(seed, shape):
     return np.random.default_rng(seed).integers(0, 256, shape, dtype=np.uint8)
+
+
+# name, seed, (H, W, C), noise amplitude, smooth -- SSIM pairs (quality.ssim_map): the test image
+# is the reference plus seeded integer noise; `smooth` images are low-frequency ramps
+SSIM_CASES = [
+    ("s_rgb_48x64", 21, (48, 64, 3), 12, False),
+    ("s_gray_40x33", 22, (40, 33, 1), 30, True),
+    ("s_rgb_min_11x11", 23, (11, 11, 3), 5, False),
+    ("s_rgb_11x40", 24, (11, 40, 3), 9, True),
+    ("s_rgb_identical_32x32", 25, (32, 32, 3), 0, True),
+    ("s_rgb_1080p", 26, (1080, 1920, 3), 20, True),
+]
+SSIM_MEAN_CASE = ("s_mean_3pairs", (27, 28, 29), (57, 71, 3), 15, True)
+
+
+def ssim_pair(seed, shape, amp, smooth):
+    rng = np.random.default_rng(seed)
+    h, w, c = shape
+    if smooth:
+        yy, xx = np.mgrid[0:h, 0:w]
+        base = 127.5 + 100.0 * np.sin(xx / 9.0 + seed) * np.cos(yy / 7.0)
+        ref = np.clip(base[..., None] + rng.integers(-8, 9, (h, w, c)), 0, 255).astype(np.uint8)
+    else:
+        ref = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    noise = rng.integers(-amp, amp + 1, (h, w, c)) if amp else 0
+    test = np.clip(ref.astype(np.int64) + noise, 0, 255).astype(np.uint8)
+    return ref, test
