@@ -203,13 +203,9 @@ __device__ __forceinline__ void h_part(uint32_t trow, uint32_t wts, int nchunk,
  * the ring wraps inside the turn.
  */
 __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row0, int cap,
-                                          uint32_t wts, int nchunk, float (&acc)[kRV][kC])
+                                          uint32_t wts, int nchunk, int zpad, float (&acc)[kRV][kC])
 {
     float win[kC][16];
-#pragma unroll
-    for (int j = 0; j < kRV; j++)
-#pragma unroll
-        for (int k = 0; k < kC; k++) acc[j][k] = 0.0f;
     const uint32_t end = col + 4u * (uint32_t)cap;
     auto step = [&](uint32_t x) {
         x += 16;
@@ -230,11 +226,7 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
     }
     float4 g4 = lds128(wts);
     uint32_t wa = wts + 16;
-    /* one chunk of four taps at ring phase p; `la` = address of the quad of rows to load */
-    auto chunk = [&](const int p, const uint32_t la) {
-        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
-        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
-        wa += 16;
+    auto refill = [&](const int p, const uint32_t la) { /* ring slot p + 3 <- the quad at la */
 #pragma unroll
         for (int k = 0; k < kC; k++) {
             const float4 x = lds128(la + k * cpitch);
@@ -243,6 +235,13 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
             win[k][(4 * (p + 3) + 2) % 16] = x.z;
             win[k][(4 * (p + 3) + 3) % 16] = x.w;
         }
+    };
+    /* one chunk of four taps at ring phase p; `la` = address of the quad of rows to load */
+    auto chunk = [&](const int p, const uint32_t la) {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
+        wa += 16;
+        refill(p, la);
 #pragma unroll
         for (int t = 0; t < 4; t++) {
 #pragma unroll
@@ -252,7 +251,38 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
                     acc[j][k] = fmaf(g[t], win[k][(4 * p + t + j) % 16], acc[j][k]);
         }
     };
-    for (int c = 0; c < nchunk; c += 4) {
+    /* The first chunk (ring phase 0) holds the zpad zeros the taps are padded with in FRONT
+     * (3 or 1: L is odd): their FMAs are skipped and the first real tap is a plain product,
+     * which is what fmaf(g, x, 0) rounds to -- no accumulator is zeroed and no zero tap is
+     * ever multiplied.  The window is unchanged: the intermediate is stored zpad rows down,
+     * so that the padded filter still starts on a quad of rows. */
+    {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa);
+        wa += 16;
+        refill(0, a);
+        if (zpad == 3) {
+#pragma unroll
+            for (int j = 0; j < kRV; j++)
+#pragma unroll
+                for (int k = 0; k < kC; k++) acc[j][k] = g[3] * win[k][(3 + j) % 16];
+        } else {
+#pragma unroll
+            for (int j = 0; j < kRV; j++)
+#pragma unroll
+                for (int k = 0; k < kC; k++) acc[j][k] = g[1] * win[k][(1 + j) % 16];
+#pragma unroll
+            for (int t = 2; t < 4; t++) {
+#pragma unroll
+                for (int j = 0; j < kRV; j++)
+#pragma unroll
+                    for (int k = 0; k < kC; k++)
+                        acc[j][k] = fmaf(g[t], win[k][(t + j) % 16], acc[j][k]);
+            }
+        }
+        a = step(a);
+    }
+    for (int c = 1; c < nchunk; c += 4) {
         /* the four load addresses of this turn: plain offsets unless the ring wraps in it */
         uint32_t a1 = a + 16, a2 = a + 32, a3 = a + 48, an = a + 64;
         if (an >= end) {
@@ -261,13 +291,13 @@ __device__ __forceinline__ void v_task_px(uint32_t col, uint32_t cpitch, int row
             a3 = step(a2);
             an = step(a3);
         }
-        chunk(0, a);
+        chunk(1, a);
         if (c + 1 >= nchunk) break;
-        chunk(1, a1);
+        chunk(2, a1);
         if (c + 2 >= nchunk) break;
-        chunk(2, a2);
+        chunk(3, a2);
         if (c + 3 >= nchunk) break;
-        chunk(3, a3);
+        chunk(0, a3);
         a = an;
     }
 }
@@ -438,16 +468,18 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
             tma_load_3d(raw + p * kPanelBytes, &tmap, bar, c0a + p * kPanelB, ys_c, g.f);
     };
     /* Zero-padded taps of an item into one of THIS WARP's two tap buffers with cp.async
-     * (src-size 0 writes the zero padding). */
+     * (src-size 0 writes the zero padding).  The padding to a multiple of four goes in FRONT
+     * (v_task_px skips it in its first chunk). */
     auto fill_taps = [&](const uint4 q, int slot) {
         const int L = (int)((q.z >> 8) & 0x1fffu);
         const int n = 4 * ((L + 3) >> 2) + 4;
+        const int z = n - 4 - L; /* zeros in front (3 or 1), one zero quad behind */
         const float *taps = pd.taps + q.w;
         float *dst = wts + (warp * 3 + slot) * wts_floats;
         for (int i = lane; i < n; i += 32) {
-            const int in_range = i < L;
+            const int in_range = i >= z && i < z + L;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
-                         "l"(taps + (in_range ? i : 0)), "r"(in_range ? 4 : 0)
+                         "l"(taps + (in_range ? i - z : 0)), "r"(in_range ? 4 : 0)
                          : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -477,16 +509,18 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
         if (tid == 0) next_slot[par] = 2 * stride + atomicAdd(cursor, 1); /* read after barrier A */
         const bool have_next = idx_nxt < n_items;
         const float *w_cur = wts + (warp * 3 + wslot) * wts_floats; /* taps, V pass */
-        const float *w_h = w_cur;                                    /* taps, H pass */
+        float *w_h = wts + (warp * 3 + 2) * wts_floats;             /* taps, H pass */
         /* this item's taps were requested one item ago by this warp */
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
-        if (sizeof(T) == 1) { /* scaled copy for the H pass (see bytes_to_float4_s) */
-            float *hb = wts + (warp * 3 + 2) * wts_floats;
+        int zpad;
+        { /* the H pass's copy: padded at the END (its window loads are tied to the tile's
+             16-byte grid), scaled for uint8 frames (see bytes_to_float4_s) */
             const int L = (int)((q_cur.z >> 8) & 0x1fffu);
             const int n = 4 * ((L + 3) >> 2) + 4;
-            for (int i = lane; i < n; i += 32) hb[i] = w_cur[i] * kTapScaleH;
-            w_h = hb;
+            zpad = n - 4 - L;
+            const float sc = sizeof(T) == 1 ? kTapScaleH : 1.0f;
+            for (int i = lane; i < n; i += 32) w_h[i] = i < L ? w_cur[i + zpad] * sc : 0.0f;
             __syncwarp();
         }
         /* request the next item's: that buffer held the previous item's taps */
@@ -678,7 +712,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                     h_part(tile_s + 4u * (uint32_t)(hrow * twp + kSegF * hset),
                            smem_u32(w_h) + 16u * (uint32_t)c0, nch, hacc);
                 if (pn == npan - 1 && hdo) {
-                    int rr = rbm + hrow;
+                    int rr = rbm + hrow + zpad; /* zpad rows down: see v_task_px */
                     rr = rr >= icap ? rr - icap : rr;
                     float *rp = ring + (size_t)(kSegF * hset) * ipitch + rr;
 #pragma unroll
@@ -716,7 +750,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         while (r0 >= icap) r0 -= icap;
                         float acc[kRV][C];
                         v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
-                                  4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, acc);
+                                  4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, zpad, acc);
                         T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
@@ -775,7 +809,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr)
  * row.  `row_s` is the shared address of the row inside chunk 0 of the block, b0 the byte of
  * the row (from the start of chunk 0) that is input 0 of this task.
  */
-__device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, int nchunk,
+__device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, int nchunk, int zpad,
                                         float (&acc)[kSegF])
 {
     constexpr int C = kC, NW = 16 * C;
@@ -812,20 +846,23 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
     uint32_t n0 = next_word(10), n1 = next_word(11), n2 = next_word(0);
     float4 g4 = lds128(wts);
     uint32_t wa = wts + 16;
-    auto chunk = [&](const int p) {
-        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
-        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
-        wa += 16;
-        /* slot p+3 <- the three words loaded during the previous chunk */
+    /* slot p+3 <- the three words loaded during the previous chunk, then load the next three:
+     * stream indices 13 + 3c .. 15 + 3c = (1 + 3p) .. (3 + 3p) mod 12 */
+    auto refill = [&](const int p) {
         const int q = ((p + 3) % 4) * 4 * C;
         put(q + 0, carry, n0);
         put(q + 4, n0, n1);
         put(q + 8, n1, n2);
         carry = n2;
-        /* the next three words: stream indices 13 + 3c .. 15 + 3c = (1 + 3p) .. (3 + 3p) mod 12 */
         n0 = next_word((1 + 3 * p) % 12);
         n1 = next_word((2 + 3 * p) % 12);
         n2 = next_word((3 + 3 * p) % 12);
+    };
+    auto chunk = [&](const int p) {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
+        wa += 16;
+        refill(p);
 #pragma unroll
         for (int t = 0; t < 4; t++) {
 #pragma unroll
@@ -833,14 +870,35 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
                 acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
         }
     };
-    for (int c = 0; c < nchunk; c += 4) {
-        chunk(0);
-        if (c + 1 >= nchunk) break;
+    /* first chunk: the taps are padded with zpad zeros in FRONT (the stream starts 3 zpad
+     * bytes early); their FMAs are skipped and the first real tap is a plain product (what
+     * fmaf(g, x, 0) rounds to), so no accumulator is zeroed -- see v_task_px */
+    {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa);
+        wa += 16;
+        refill(0);
+        if (zpad == 3) {
+#pragma unroll
+            for (int j = 0; j < kSegF; j++) acc[j] = g[3] * win[(C * 3 + j) % NW];
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSegF; j++) acc[j] = g[1] * win[(C * 1 + j) % NW];
+#pragma unroll
+            for (int t = 2; t < 4; t++) {
+#pragma unroll
+                for (int j = 0; j < kSegF; j++) acc[j] = fmaf(g[t], win[(C * t + j) % NW], acc[j]);
+            }
+        }
+    }
+    for (int c = 1; c < nchunk; c += 4) {
         chunk(1);
-        if (c + 2 >= nchunk) break;
+        if (c + 1 >= nchunk) break;
         chunk(2);
-        if (c + 3 >= nchunk) break;
+        if (c + 2 >= nchunk) break;
         chunk(3);
+        if (c + 3 >= nchunk) break;
+        chunk(0);
     }
 }
 
@@ -877,7 +935,8 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
      * source row clamped into the image. */
     auto issue = [&](const uint4 q, int rb) {
         const item_geo g = decode_item<C>(q, W);
-        const int byte0 = (g.x0 - g.r) * C;
+        /* the H pass's stream starts 3 zpad bytes left of the tile (front-padded taps) */
+        const int byte0 = (g.x0 - g.r) * C - C * (4 * g.nchunk - g.L);
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
         mbar_expect_tx(bar, (uint32_t)(nq * kQStride));
         tma_load_4d(raw, &tmap, bar, 0, ys_c, byte0 >> 4, g.f);
@@ -885,12 +944,13 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
     auto fill_taps = [&](const uint4 q, int slot) {
         const int L = (int)((q.z >> 8) & 0x1fffu);
         const int n = 4 * ((L + 3) >> 2) + 4;
+        const int z = n - 4 - L; /* zeros in front (3 or 1), one zero quad behind */
         const float *taps = pd.taps + q.w;
         float *dst = wts + (warp * 3 + slot) * wts_floats;
         for (int i = lane; i < n; i += 32) {
-            const int in_range = i < L;
+            const int in_range = i >= z && i < z + L;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)),
-                         "l"(taps + (in_range ? i : 0)), "r"(in_range ? 4 : 0)
+                         "l"(taps + (in_range ? i - z : 0)), "r"(in_range ? 4 : 0)
                          : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -939,8 +999,10 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
         const item_geo g = decode_item<C>(q_cur, W);
         const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
         const int nchunk = g.nchunk, th = g.th, tw = g.tw;
+        const int zpad = 4 * nchunk - g.L; /* zeros in front of the taps: 3 or 1 */
         T *dst = out + (size_t)g.f * H * W * C;
-        const int skew = ((x0 - r) * C) & 15;                      /* tile float 0 = raw byte skew */
+        const int skew_h = ((x0 - r) * C - C * zpad) & 15;         /* the stream's byte 0 in the box */
+        const int skew = skew_h + C * zpad;                        /* tile float 0 = raw byte skew */
         const int nl = r - x0 > 0 ? r - x0 : 0;                    /* tile pixels left of the image */
         const int nr = x0 + fw + r - W > 0 ? x0 + fw + r - W : 0; /* ... and right of it */
         const int ncol = fw * C - kSegF * warp < kSegF ? fw * C - kSegF * warp : kSegF;
@@ -994,12 +1056,10 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
              * box row it reads), the warp's 24 columns */
             if (active && lane < nrows) {
                 float hacc[kSegF];
-#pragma unroll
-                for (int j = 0; j < kSegF; j++) hacc[j] = 0.0f;
                 const int brow = fast_clamp(ys + lane, 0, H - 1) - ys_c; /* box row */
-                h_bytes(raw_s + (uint32_t)(brow * kQB), skew + kSegF * warp, smem_u32(w_h), nchunk,
-                        hacc);
-                int rr = rbm + lane;
+                h_bytes(raw_s + (uint32_t)(brow * kQB), skew_h + kSegF * warp, smem_u32(w_h), nchunk,
+                        zpad, hacc);
+                int rr = rbm + lane + zpad; /* zpad rows down: see v_task_px */
                 rr = rr >= icap ? rr - icap : rr;
                 float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
 #pragma unroll
@@ -1046,7 +1106,7 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
                         while (r0 >= icap) r0 -= icap;
                         float acc[kRV][C];
                         v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
-                                  4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, acc);
+                                  4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, zpad, acc);
                         T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px;
 #pragma unroll
                         for (int j = 0; j < kRV; j++) {
