@@ -1250,11 +1250,11 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
     CUtensorMap map;
     memset(&map, 0, sizeof map);
     if (is_f32) return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
-    /* uint8 by TMA: the classes with long filters (2 and up) run the kernel whose H pass reads
-     * the TMA bytes directly -- no working tile, so 4 or 3 CTAs per SM where fk_blur_cols has 2;
-     * the short-filter classes are a little faster with the converted tile.  Variant 4: fk_blur_cols
-     * everywhere, variant 5: fk_blur_bytes everywhere. */
-    if (h->variant == 5 || (h->variant == 0 && klass >= 2)) {
+    /* uint8 by TMA: fk_blur_bytes, the kernel whose H pass reads the TMA bytes directly -- no
+     * working tile, no conversion pass, no CTA barrier, 4 CTAs per SM up to 69 taps and 3 up
+     * to 105.  (Until the taps were padded in front it only won for the long filters.)
+     * Variant 4: fk_blur_cols for every class, variant 5: same as the default. */
+    if (h->variant == 5 || h->variant == 0) {
         cudaError_t e = launch_bytes(h, pd, klass, in, out, n_frames, class_length, s, taken);
         if (e != cudaSuccess || *taken) return e;
     }
