@@ -34,7 +34,7 @@ enum {
  * fits its longest filter.  Inside a list, a frame's items are contiguous.
  */
 #define FK_RECT 32
-#define FK_STRIP_ROWS 256
+#define FK_STRIP_ROWS 512
 #define FK_NCLASS 7
 /* Classes 0..4 are rendered by the fast kernels, each launch with the shared-memory layout
  * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_bytes (4 resident CTAs
