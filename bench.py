@@ -313,8 +313,9 @@ def run_gpu(args):
         pass
     roofline = {
         "bound": "fp32" if t_fp32 >= t_hbm else "hbm",
-        "kernel": ("fk_blur_bytes + fk_blur_cols (render of the whole batch: one persistent "
-                   "launch per tap-count class, up to 4 per step; timed together)"),
+        "kernel": (("fk_blur_bytes" if args.dtype == "u8" else "fk_blur_cols") +
+                   " (render of the whole batch: one persistent launch per tap-count class, up "
+                   "to 5 per step, side by side on forked streams; timed together)"),
         "achieved": achieved_tf, "peak": fp32_nominal, "unit": "TFLOP/s",
         "frac": achieved_tf / fp32_nominal,
         "peak_source": (f"nominal FP32 = 2 x {eng.info['sm_count']} SMs x 128 lanes x "

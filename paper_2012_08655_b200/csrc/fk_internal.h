@@ -34,7 +34,7 @@ enum {
  * fits its longest filter.  Inside a list, a frame's items are contiguous.
  */
 #define FK_RECT 32
-#define FK_STRIP_ROWS 512
+#define FK_STRIP_ROWS 1024
 #define FK_NCLASS 7
 /* Classes 0..4 are rendered by the fast kernels, each launch with the shared-memory layout
  * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_bytes (4 resident CTAs
@@ -88,6 +88,7 @@ struct fk_plan_dev {
     int cap;             /* per-frame stride of the cell arrays */
     int nsub_x;          /* strips per fragment across: ceil(fragment / FK_RECT) */
     int nsub_y;          /* strips per fragment down: ceil(fragment / FK_STRIP_ROWS) */
+    int strip_rows;      /* tallest strip the plan kernel merges fragments into (fk_strip_rows_for) */
     size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */
     fk_item *items;      /* [FK_NCLASS][items_cap] */
     int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors */
@@ -153,6 +154,12 @@ struct fk_plan {
     size_t density_cap = 0;
     fk_plan_dev d{};
 };
+
+/* Tallest merged strip for a batch of n_frames: taller strips share more of the horizontal
+ * pass (the 2r halo rows between merged fragments) and cost fewer item set-ups, shorter ones
+ * give the persistent CTAs of a small batch enough items to share.  FK_STRIP_ROWS_FORCE in
+ * the environment overrides it (tuning runs). */
+int fk_strip_rows_for(int n_frames);
 
 /* error plumbing (fk_api.cu) */
 int fk_fail(fk_handle *h, int code, const char *fmt, ...);

@@ -61,7 +61,7 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  *   across  m = FK_RECT / F neighbouring cells of a grid row (aligned groups after the
  *           leading partial cell) become one unit FK_RECT wide when they share their taps;
  *   down    a vertical run of equal units (same cells, same taps) is cut from its top into
- *           strips of at most FK_STRIP_ROWS / F grid rows, which lets the fragments of a
+ *           strips of at most pd.strip_rows / F grid rows, which lets the fragments of a
  *           strip share the horizontal pass over the 2r halo rows between them.
  * Wider fragments are cut into columns FK_RECT wide (and pieces FK_STRIP_ROWS tall) without
  * merging across cells.
@@ -78,7 +78,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
     const int F = pd.fragment;
     const bool merge = F <= FK_RECT;
-    const int maxc = merge ? (FK_STRIP_ROWS / F > 1 ? FK_STRIP_ROWS / F : 1) : 1;
+    const int maxc = merge ? (pd.strip_rows / F > 1 ? pd.strip_rows / F : 1) : 1;
     const int mgrp = merge ? FK_RECT / F : 1; /* cells per horizontal unit */
     const int lead = sx > 0 ? 1 : 0;
     const int per_cell = merge ? 1 : pd.nsub_x * pd.nsub_y;
