@@ -1026,30 +1026,44 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
                 if (have_next) fill_taps(q_nxt, wslot ^ 1);
             }
             if (nl | nr) {
-                /* clamp-to-edge in x (blockwise.py:147): overwrite the raw bytes left and right
-                 * of the image with the edge pixel, 8 box rows per warp */
-                const int el = skew + nl * C, er = skew + (W - 1 - x0 + r) * C;
+                /* clamp-to-edge in x (blockwise.py:147): the raw bytes left and right of the
+                 * image become copies of the edge pixel.  Four lanes per box row, each one
+                 * 16-byte chunk at a time: the run is periodic in 3 bytes, so a chunk is four of
+                 * three pre-rotated words picked by the chunk's phase, merged under a byte mask
+                 * with what is there (only the chunk at the image border keeps any of it --
+                 * whatever lies beyond the tile's ends meets zero taps only). */
+                const int prow = warp * kWR + (lane >> 2);
+                unsigned char *rowp = raw + prow * kQB;
+                auto at = [&](int m) -> uint32_t { return rowp[(m >> 4) * kQStride + (m & 15)]; };
+                auto lowbytes = [](int n) { return n >= 4 ? 0xffffffffu : n <= 0 ? 0u : (1u << (8 * n)) - 1u; };
+                auto fill = [&](int e, int A, int B) { /* bytes [A, B) <- pixel at byte e */
+                    const uint32_t px = at(e) | (at(e + 1) << 8) | (at(e + 2) << 16);
+                    const uint32_t rot[3] = {__byte_perm(px, 0u, 0x0210), __byte_perm(px, 0u, 0x1021),
+                                             __byte_perm(px, 0u, 0x2102)};
 #pragma unroll 1
-                for (int i = 0; i < kWR; i++) {
-                    unsigned char *rowp = raw + (warp * kWR + i) * kQB;
-                    auto at = [&](int m) -> unsigned char & { return rowp[(m >> 4) * kQStride + (m & 15)]; };
-                    if (nl) {
-                        const unsigned char l0 = at(el), l1 = at(el + 1), l2 = at(el + 2);
-#pragma unroll 1
-                        for (int j = lane; j < nl * C; j += 32) {
-                            const int c = j % C;
-                            at(skew + j) = c == 0 ? l0 : (c == 1 ? l1 : l2);
+                    for (int q = (A >> 4) + (lane & 3); q <= (B - 1) >> 4; q += 4) {
+                        const int m0 = q * 16;
+                        int ph = (m0 - e) % 3; /* channel of the chunk's first byte */
+                        ph = ph < 0 ? ph + 3 : ph;
+                        uint4 *cp = reinterpret_cast<uint4 *>(rowp + q * kQStride);
+                        uint4 v = *cp;
+                        uint32_t *w = &v.x;
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            int f = ph + k;
+                            f = f >= 3 ? f - 3 : f;
+                            const uint32_t pat = f == 0 ? rot[0] : (f == 1 ? rot[1] : rot[2]);
+                            const uint32_t mask = lowbytes(B - m0 - 4 * k) & ~lowbytes(A - m0 - 4 * k);
+                            w[k] = (w[k] & ~mask) | (pat & mask);
                         }
+                        *cp = v;
                     }
-                    if (nr) {
-                        const unsigned char r0 = at(er), r1 = at(er + 1), r2 = at(er + 2);
-#pragma unroll 1
-                        for (int j = lane; j < nr * C; j += 32) {
-                            const int c = j % C;
-                            at(skew + tw - nr * C + j) = c == 0 ? r0 : (c == 1 ? r1 : r2);
-                        }
-                    }
-                }
+                };
+                /* the edge pixels sit on a pixel boundary of the run they feed, so e fixes the
+                 * phase; the far end of either run may be rounded out to its chunk */
+                if (nl) fill(skew + nl * C, (skew & ~15), skew + nl * C);
+                __syncwarp(); /* in a very narrow image both runs can meet in one chunk */
+                if (nr) fill(skew + (W - 1 - x0 + r) * C, skew + tw - nr * C, ((skew + tw + 15) & ~15));
                 __syncthreads();
             }
             /* horizontal pass (blockwise.py:151): lane = tile row (clamped in y through the
