@@ -377,6 +377,7 @@ __device__ __noinline__ void patch_x_edges(const unsigned char *raw, float *trow
  * row 0, `row_first` is the warp's first source row (rows clamp in y), `last` the last aligned
  * quad of an image row that may be read.
  */
+constexpr int kG = 8; /* rows a lane keeps in flight while staging float32 frames */
 template <int REM>
 __device__ __forceinline__ void stage_rows_f32(const float *__restrict__ g0, int row_first, int H,
                                                int rowstride, int aq0, int last,
@@ -388,17 +389,17 @@ __device__ __forceinline__ void stage_rows_f32(const float *__restrict__ g0, int
         const bool ok = q < nw;
         const bool okb = REM != 0 && ok && aq0 + q + 1 <= last;
 #pragma unroll 1
-        for (int i0 = 0; i0 < kWR; i0 += 4) { /* four rows in flight */
-            float4 a[4], b[4];
+        for (int i0 = 0; i0 < kWR; i0 += kG) { /* kG rows in flight */
+            float4 a[kG], b[kG];
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
+            for (int i = 0; i < kG; i++) {
                 const float4 *rp = reinterpret_cast<const float4 *>(
                                        g0 + (size_t)fast_clamp(row_first + i0 + i, 0, H - 1) * rowstride) + q;
                 a[i] = ok ? __ldg(rp) : make_float4(0.f, 0.f, 0.f, 0.f);
                 b[i] = okb ? __ldg(rp + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
+            for (int i = 0; i < kG; i++) {
                 float4 v;
                 if (REM == 0) v = a[i];
                 if (REM == 1) v = make_float4(a[i].y, a[i].z, a[i].w, b[i].x);
