@@ -1,6 +1,7 @@
 """Repeatability / agreement stress: many 1080p frames with random fixations through the default
-dispatch (fk_blur_bytes + fk_blur_cols), fk_blur_cols everywhere (variant 4) and fk_blur_bytes
-everywhere (variant 5); all runs must be bit-identical.  usage: python tools/stress_variants.py [frames] [rounds]"""
+dispatch (fk_blur_bytes, class launches side by side), fk_blur_cols everywhere (variant 4), the
+generic kernel (variant 1, first round) and the default kernels launched one class after the
+other (variant 16); all runs must be bit-identical.  usage: python tools/stress_variants.py [frames] [rounds]"""
 import sys
 
 import numpy as np
@@ -19,13 +20,13 @@ for r in range(rounds):
     fix = np.stack([rng.uniform(0, 1920, n), rng.uniform(0, 1080, n)], axis=1)
     p = fk.FoveationParams(strength=float(rng.uniform(0.6, 1.4)))
     outs = {}
-    for v in (4, 0, 5, 0):
+    for v in (4, 0, 16, 0) + ((1,) if r == 0 else ()):
         eng.set_kernel_variant(v)
         o = fk.foveate_batch(frames, fix, p)
         if v in outs:
             bad += int(not torch.equal(outs[v], o))
         outs[v] = o.clone()
     eng.set_kernel_variant(0)
-    bad += int(not torch.equal(outs[4], outs[0])) + int(not torch.equal(outs[5], outs[0]))
+    bad += sum(int(not torch.equal(outs[v], outs[0])) for v in outs if v != 0)
     print("round", r, "mismatches so far", bad, flush=True)
 print("OK" if bad == 0 else "FAILED")
