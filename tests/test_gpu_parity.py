@@ -490,3 +490,38 @@ def test_tma_path_border_and_interior_tiles_vs_generic():
         view = flat[4:4 + frames.numel()].view_as(frames)
         view.copy_(frames)
         assert torch.equal(fk.foveate_batch(view, fix, p), ref)
+
+
+@pytest.mark.gpu
+def test_strip_height_does_not_change_the_output():
+    """Merging same-filter fragments into strips is exact (an output pixel depends only on the
+    image and its filter), whatever the cap on the strip height: the batch default (1 024 rows),
+    the single-frame default (64) and no merging at all (32 = one fragment) give the same bytes.
+    FK_STRIP_ROWS_FORCE is read once per process, so each setting runs in its own."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, hashlib, numpy as np, torch\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2012_08655_b200 as fk\n"
+        "rng = np.random.default_rng(5)\n"
+        "frames = torch.from_numpy(rng.integers(0, 256, (12, 540, 960, 3), dtype=np.uint8)).cuda()\n"
+        "fix = np.stack([rng.uniform(0, 960, 12), rng.uniform(0, 540, 12)], axis=1)\n"
+        "out = fk.foveate_batch(frames, fix, fk.FoveationParams(fragment_size=32, strength=1.3))\n"
+        "print(hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = {}
+    for force in ("", "32", "64", "1024"):
+        env = dict(os.environ)
+        env.pop("FK_STRIP_ROWS_FORCE", None)
+        if force:
+            env["FK_STRIP_ROWS_FORCE"] = force
+        res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        digests[force] = res.stdout.strip().splitlines()[-1]
+    assert len(set(digests.values())) == 1, digests
