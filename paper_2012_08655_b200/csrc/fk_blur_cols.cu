@@ -903,7 +903,10 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+/* Three resident CTAs per SM with 167 registers beat four with 127 (27.0 k against 26.8 k
+ * frames/s on the bench, 19.4 k against 18.8 k with corner fixations): at 127 the compiler
+ * rematerialises addresses and constants inside the task set-up. */
+__global__ void __launch_bounds__(kThreads, 3)
 fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t *__restrict__ out,
               int klass, int wts_floats, int nq, int icap, int ipitch)
 {
@@ -1266,8 +1269,7 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
     memset(&map, 0, sizeof map);
     if (is_f32) return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
     /* uint8 by TMA: fk_blur_bytes, the kernel whose H pass reads the TMA bytes directly -- no
-     * working tile, no conversion pass, no CTA barrier, 4 CTAs per SM up to 69 taps and 3 up
-     * to 105.  (Until the taps were padded in front it only won for the long filters.)
+     * working tile, no conversion pass, no CTA barrier, 3 CTAs per SM up to 105 taps.  (Until the taps were padded in front it only won for the long filters.)
      * Variant 4: fk_blur_cols for every class, variant 5: same as the default. */
     if (h->variant == 5 || h->variant == 0) {
         cudaError_t e = launch_bytes(h, pd, klass, in, out, n_frames, class_length, s, taken);

@@ -37,9 +37,9 @@ enum {
 #define FK_STRIP_ROWS 1024
 #define FK_NCLASS 7
 /* Classes 0..4 are rendered by the fast kernels, each launch with the shared-memory layout
- * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_bytes (4 resident CTAs
- * per SM up to 69 taps, 3 up to 89 -- and up to 105 when the batch has nothing longer -- 2 up
- * to 127).  Everything else (float32 frames, buffers TMA cannot describe): fk_blur_cols, 3
+ * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_bytes (3 resident CTAs
+ * per SM -- its register budget -- up to 89 taps, and up to 105 when the batch has nothing
+ * longer; 2 up to 127).  Everything else (float32 frames, buffers TMA cannot describe): fk_blur_cols, 3
  * CTAs per SM in classes 0 and 1, 2 in classes 2 and 3 with a whole-width working tile and in
  * class 4 with the taps walked in panels.  Class 5 (longer filters) goes to the generic
  * kernel, class 6 holds the identity fragments (L = 1), plain copies. */
