@@ -908,20 +908,23 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
  * rematerialises addresses and constants inside the task set-up. */
 __global__ void __launch_bounds__(kThreads, 3)
 fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t *__restrict__ out,
-              int klass, int wts_floats, int nq, int icap, int ipitch)
+              int klass, int wts_floats, int nq, int icap, int ipitch, int nbuf)
 {
     constexpr int C = kC;
     typedef uint8_t T;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw: nq chunks x 32 rows x 16 B][barriers + item slots, 128 B][per-warp taps x 3][ring] */
-    unsigned char *raw = smem_raw;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + nq * kQStride);
-    uint64_t *hbar = bar + 1;
-    int *slot_idx = reinterpret_cast<int *>(bar + 2);                 /* [2] */
-    uint4 *slot_desc = reinterpret_cast<uint4 *>(bar + 4);            /* [2], 16-byte aligned */
+    /* layout: [raw x nbuf: nq chunks x 32 rows x 16 B][barriers + item slots, 128 B][per-warp taps x 3][ring]
+     * nbuf = 2 where a second raw buffer does not cost a resident CTA: the TMA request then
+     * runs two blocks ahead of the H pass instead of one, so the first blocks of an item --
+     * which have no V pass yet to hide the fetch under -- do not wait for their bytes. */
+    const int raw_bytes = nq * kQStride;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + nbuf * raw_bytes); /* [2] bytes landed */
+    uint64_t *hbar = bar + 2;                                                   /* [2] H pass done */
+    int *slot_idx = reinterpret_cast<int *>(bar + 4);                 /* [2] */
+    uint4 *slot_desc = reinterpret_cast<uint4 *>(bar + 6);            /* [2], 16-byte aligned */
     float *wts = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(bar) + 128);
     float *ring = wts + kWarps * 3 * wts_floats;
-    const uint32_t ring_s = smem_u32(ring), raw_s = smem_u32(raw);
+    const uint32_t ring_s = smem_u32(ring);
 
     const int W = pd.width, H = pd.height;
     const int tid = threadIdx.x;
@@ -937,13 +940,12 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
     /* One 32-row block: the box starts at the 16-byte chunk that holds the tile's first byte
      * (possibly left of the image: TMA fills what is outside with zeros) and at the first
      * source row clamped into the image. */
-    auto issue = [&](const uint4 q, int rb) {
-        const item_geo g = decode_item<C>(q, W);
+    auto issue = [&](const item_geo &g, int rb, int buf) {
         /* the H pass's stream starts 3 zpad bytes left of the tile (front-padded taps) */
         const int byte0 = (g.x0 - g.r) * C - C * (4 * g.nchunk - g.L);
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
-        mbar_expect_tx(bar, (uint32_t)(nq * kQStride));
-        tma_load_4d(raw, &tmap, bar, 0, ys_c, byte0 >> 4, g.f);
+        mbar_expect_tx(bar + buf, (uint32_t)raw_bytes);
+        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, byte0 >> 4, g.f);
     };
     auto fill_taps = [&](const uint4 q, int slot) {
         const int L = (int)((q.z >> 8) & 0x1fffu);
@@ -969,21 +971,48 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
     uint4 q_nxt = load_item(idx_nxt);
     if (tid == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         mbar_init(hbar, kWarps);
+        mbar_init(hbar + 1, kWarps);
     }
     for (int i = tid; i < kRowF * ipitch / 4; i += kThreads)
         reinterpret_cast<float4 *>(ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (idx < n_items) fill_taps(q_cur, 0);
     __syncthreads();
-    if (tid == 0 && idx < n_items) issue(q_cur, 0);
 
-    uint32_t phase = 0, hphase = 0;
+    /* Thread 0's request cursor: the block to fetch next -- item `cq`, tile row `crb` -- runs
+     * nbuf blocks ahead of the H pass and `clead` items ahead of the item loop (every item has
+     * at least two blocks, so at most two: the next item, or the one drawn for after it). */
+    int d_idx = n_items;
+    uint4 d_q = none;
+    uint4 cq = q_cur;
+    bool cvalid = idx < n_items;
+    int crb = 0, clead = 0, ibuf = 0;
+    auto request_next = [&]() {
+        if (!cvalid) return;
+        const item_geo g = decode_item<C>(cq, W);
+        const int lead = (2 * g.r) & (kTB - 1);
+        const int n_first = lead == 0 || lead > g.th ? (g.th < kTB ? g.th : kTB) : lead;
+        const int nrows = crb == 0 ? n_first : (g.th - crb < kTB ? g.th - crb : kTB);
+        issue(g, crb, ibuf);
+        ibuf ^= nbuf - 1;
+        crb += nrows;
+        if (crb >= g.th) { /* on to the following item */
+            crb = 0;
+            clead++;
+            cq = clead == 1 ? q_nxt : d_q;
+            cvalid = (clead == 1 ? idx_nxt : d_idx) < n_items;
+        }
+    };
+    if (tid == 0)
+        for (int i = 0; i < nbuf; i++) request_next();
+
+    int bc = 0; /* blocks this CTA has been through: buffer bc % nbuf, its phase (bc / nbuf) & 1 */
     int wslot = 0, par = 0, item_no = 0;
     for (; idx < n_items; idx = idx_nxt, q_cur = q_nxt, wslot ^= 1, par ^= 1, item_no++) {
         /* thread 0: draw the item after the next and start fetching its descriptor */
-        int d_idx = n_items;
-        uint4 d_q = none;
         bool d_pending = false;
+        if (item_no > 0 && clead > 0) clead--;
         if (tid == 0) {
             d_idx = 2 * stride + atomicAdd(cursor, 1);
             d_q = load_item(d_idx);
@@ -1019,8 +1048,12 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
         for (int rb = 0, nrows = n_first; rb < th; rb += nrows, nrows = th - rb < kTB ? th - rb : kTB) {
             const int ys = y0 - r + rb;
             const int ys_c = fast_clamp(ys, 0, H - 1);
-            mbar_wait(bar, phase); /* the block's bytes have landed */
-            phase ^= 1;
+            const int buf = bc & (nbuf - 1);
+            const uint32_t phase = (uint32_t)((nbuf == 2 ? bc >> 1 : bc) & 1);
+            unsigned char *raw = smem_raw + buf * raw_bytes;
+            const uint32_t raw_s = smem_u32(raw);
+            bc++;
+            mbar_wait(bar + buf, phase); /* the block's bytes have landed */
             if (rb == 0) {
                 if (item_no > 0) { /* the next item, published by thread 0 during the previous one */
                     idx_nxt = slot_idx[par ^ 1];
@@ -1084,11 +1117,11 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
                 for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(hbar); /* this warp is through with the raw bytes */
+            if (lane == 0) mbar_arrive(hbar + buf); /* this warp is through with the raw bytes */
             if (warp == 0) {
-                /* every warp is through: publish the drawn item, then the next block's (or the
-                 * next item's first) bytes */
-                mbar_wait(hbar, hphase);
+                /* every warp is through with this buffer: publish the drawn item, then request
+                 * the block nbuf ahead into it */
+                mbar_wait(hbar + buf, phase);
                 if (lane == 0) {
                     if (d_pending) {
                         slot_idx[par] = d_idx;
@@ -1098,11 +1131,9 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
                                                   other warps read the slot after they have
                                                   seen bytes that request brought in */
                     }
-                    const bool more = rb + nrows < th;
-                    if (more || have_next) issue(more ? q_cur : q_nxt, more ? rb + nrows : 0);
+                    request_next();
                 }
             }
-            hphase ^= 1;
             rbm += nrows;
             while (rbm >= icap) rbm -= icap;
 
@@ -1237,8 +1268,8 @@ cudaError_t launch_bytes(fk_handle *h, const fk_plan_dev &pd, int klass, const v
     const int nq = (168 + 6 * r + kQB - 1) / kQB; /* chunks a lane's word stream can reach */
     const int icap = (2 * r + kTB + 3) & ~3;
     const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
-    const size_t smem = (size_t)nq * kQStride + 128 +
-                        ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
+    size_t smem = (size_t)nq * kQStride + 128 +
+                  ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
     if (smem > h->prop.sharedMemPerBlockOptin) return cudaSuccess;
     CUtensorMap map;
     memset(&map, 0, sizeof map);
@@ -1250,8 +1281,23 @@ cudaError_t launch_bytes(fk_handle *h, const fk_plan_dev &pd, int klass, const v
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaSuccess;
+    /* a second raw buffer where it does not cost a resident CTA (variant 6: never) */
+    int nbuf = 1;
+    const size_t smem2 = smem + (size_t)nq * kQStride;
+    if (smem2 <= h->prop.sharedMemPerBlockOptin && h->variant != 6) {
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        if (e != cudaSuccess) return e;
+        int occ2 = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, kernel, kThreads, smem2);
+        if (e != cudaSuccess) return e;
+        if (occ2 >= occ) {
+            nbuf = 2;
+            smem = smem2;
+        }
+    }
     const int grid = h->prop.multiProcessorCount * occ;
-    kernel<<<grid, kThreads, smem, s>>>(map, pd, (uint8_t *)out, klass, wts_floats, nq, icap, ipitch);
+    kernel<<<grid, kThreads, smem, s>>>(map, pd, (uint8_t *)out, klass, wts_floats, nq, icap, ipitch,
+                                        nbuf);
     *taken = true;
     return cudaGetLastError();
 }
@@ -1271,7 +1317,7 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
     /* uint8 by TMA: fk_blur_bytes, the kernel whose H pass reads the TMA bytes directly -- no
      * working tile, no conversion pass, no CTA barrier, 3 CTAs per SM up to 105 taps.  (Until the taps were padded in front it only won for the long filters.)
      * Variant 4: fk_blur_cols for every class, variant 5: same as the default. */
-    if (h->variant == 5 || h->variant == 0) {
+    if (h->variant == 5 || h->variant == 0 || h->variant == 6) { /* 6: one raw buffer */
         cudaError_t e = launch_bytes(h, pd, klass, in, out, n_frames, class_length, s, taken);
         if (e != cudaSuccess || *taken) return e;
     }
