@@ -1,6 +1,8 @@
 /*
- * fk_blur_cols.cu -- column-partitioned separable blur for RGB frames on sm_100a (the hot
- * kernel of the render path).
+ * fk_blur_cols.cu -- column-partitioned separable blur for RGB frames on sm_100a: fk_blur_cols
+ * (float32 frames, and uint8 buffers TMA cannot describe) and, further down, fk_blur_bytes --
+ * the hot kernel of the render path, uint8 frames by TMA -- which shares everything after the
+ * H pass with it.
  *
  * Same arithmetic as blockwise.py:136-153 (_render_cell): clamp-to-edge tile, horizontal
  * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
@@ -43,8 +45,10 @@
  * accumulators of a lane's row stay in registers across panels (same taps, same order: the
  * result does not change), and each panel costs one more pair of barriers.
  *
- * Taps are zero-padded to a multiple of 4; every shared-memory word a padded tap can touch
- * holds a finite value so 0 * garbage never produces a NaN.
+ * Taps are zero-padded to a multiple of 4 -- in FRONT for the V pass and for the H pass of
+ * fk_blur_bytes, whose first chunk skips the zeros and starts from a plain product (see
+ * v_task_px), at the end for h_part; every shared-memory word a padded tap can touch holds a
+ * finite value so 0 * garbage never produces a NaN.
  */
 #include "fk_stage.cuh"
 
@@ -783,8 +787,9 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
  * registers and bumps each after use.  Rows clamp in y by picking the box row; columns
  * outside the image are patched in the raw bytes (edge items only, with a CTA barrier).
  * Everything after the H pass (transposed intermediate, V pass, dealing of items, taps) is
- * fk_blur_cols.  Synchronisation: `bar` (TMA bytes landed, all warps wait) and `hbar` ("H pass
- * done", one arrival per warp; thread 0 waits for it before it issues the next block's TMA).
+ * fk_blur_cols.  Synchronisation: per raw buffer (one or two) a `bar` (TMA bytes landed, all
+ * warps wait) and an `hbar` ("H pass done", one arrival per warp; thread 0 waits for it before
+ * it requests the block that goes into that buffer next).
  * ===================================================================================== */
 constexpr int kQB = 16;            /* bytes per chunk */
 constexpr int kQStride = kQB * kTB; /* bytes between chunks in shared memory: 512 */
