@@ -149,9 +149,17 @@ int fk_plan_read(fk_plan *p, int frame, fk_plan_view *out, void *stream);
 int fk_plan_read_lengths(fk_plan *p, int first, int count, int32_t *lengths_host,
                          int32_t *meta_host, void *stream);
 
+/* Frames of the last fk_plan_model / fk_plan_density call whose fixation lies outside the
+ * image or is not a number (retinal.py:73-74 raises ValueError("fixation ... outside image")).
+ * Host fixations are rejected before anything is launched; fixations that are already on
+ * the device can only be checked there: the plan kernel counts them, copies those frames
+ * through unchanged and this call reads the count (synchronises the stream). */
+int fk_plan_status(fk_plan *p, int *bad_frames, void *stream);
+
 /* ---- render: the per-fragment separable blur -------------------------------------- */
 /* Replaces render / _render_cell (blockwise.py:136-186) + quantize_u8 (convolve.py:9-15)
- * for n_frames frames planned in `p`.  in/out are device pointers, [n][H][W][C]. */
+ * for the n_frames frames planned in `p` (n_frames must equal the planned count: the work
+ * lists cover every planned frame).  in/out are device pointers, [n][H][W][C]. */
 int fk_render_u8(fk_handle *h, const fk_plan *p, const uint8_t *in_dev, uint8_t *out_dev,
                  int n_frames, int channels, void *stream);
 /* Same arithmetic on float32 frames, result left unquantised (BASELINE config 5). */

@@ -211,7 +211,8 @@ def _check_fixations(fix, n, size):
 
 
 def foveate_batch(frames, fixations=None, params: FoveationParams | None = None, *, out=None,
-                  devices=None, use_shift: bool = True, chunk_frames: int = 0):
+                  devices=None, use_shift: bool = True, chunk_frames: int = 0,
+                  validate: bool = True):
     """Foveate a batch of frames, one fixation per frame.
 
     frames     [N, H, W, C] uint8 or float32, C in {1, 3}: a numpy array (host memory,
@@ -222,6 +223,9 @@ def foveate_batch(frames, fixations=None, params: FoveationParams | None = None,
                float64 tensor.
     devices    GPUs to shard host batches over (contiguous split of N, no collective:
                frames are independent).  Default: the current device only.
+    validate   device fixations only: read the plan kernel's out-of-image count back and
+               raise ValueError like the reference (synchronises); False keeps the call
+               asynchronous and copies such frames through.
     """
     params = params if params is not None else FoveationParams()
     if isinstance(frames, torch.Tensor) and frames.is_cuda:
@@ -232,7 +236,8 @@ def foveate_batch(frames, fixations=None, params: FoveationParams | None = None,
             fixations = _check_fixations(fixations, n, (w, h))
         eng = get_engine(frames.device.index)
         with torch.cuda.device(eng.device):
-            res, _ = eng.foveate_device(frames, fixations, params, use_shift=use_shift, out=out)
+            res, _ = eng.foveate_device(frames, fixations, params, use_shift=use_shift, out=out,
+                                        validate=validate)
         return res
 
     if isinstance(frames, torch.Tensor):

@@ -290,7 +290,7 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
     if (e == cudaSuccess) e = cudaMalloc(&d.offset, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.strip, cells * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.items, FK_NCLASS * d.items_cap * sizeof(fk_item));
-    if (e == cudaSuccess) e = cudaMalloc(&d.counters, 2 * FK_NCLASS * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.counters, FK_COUNTER_WORDS * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&d.meta, (size_t)max_frames * FK_META_WORDS * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&p->fix_dev, (size_t)max_frames * 2 * sizeof(double));
     if (e != cudaSuccess) {
@@ -376,7 +376,7 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     }
     p->d.taps = h->lut32;
     p->custom = 0;
-    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
+    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev no_density = {nullptr, 0, 0, 0.0};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, no_density, s));
@@ -441,7 +441,7 @@ int fk_plan_density(fk_plan *p, const fk_params *prm, int n_frames, const double
     }
     p->d.taps = h->lut32;
     p->custom = 0;
-    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
+    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev den = {p->density_map, map_w, map_h, sigma_max};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, den, s));
@@ -502,7 +502,7 @@ int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_
     FK_CUDA(h, cudaStreamSynchronize(s));
     p->d.taps = p->custom_taps;
     p->custom = 1;
-    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t), s));
+    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     p->d.strip_rows = fk_strip_rows_for(1);
     FK_CUDA(h, fk_launch_order_custom(p->d, s));
     h->launches++;
@@ -564,6 +564,21 @@ int fk_plan_read(fk_plan *p, int frame, fk_plan_view *out, void *stream)
     return FK_OK;
 }
 
+int fk_plan_status(fk_plan *p, int *bad_frames, void *stream)
+{
+    if (!p || !bad_frames) return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");
+    fk_handle *h = p->h;
+    *bad_frames = 0;
+    if (p->n_frames < 1) return FK_OK;
+    FK_CUDA(h, cudaSetDevice(h->device));
+    int32_t bad = 0;
+    FK_CUDA(h, cudaMemcpyAsync(&bad, p->d.counters + FK_COUNTER_BAD, sizeof bad,
+                               cudaMemcpyDeviceToHost, as_stream(stream)));
+    FK_CUDA(h, cudaStreamSynchronize(as_stream(stream)));
+    *bad_frames = bad;
+    return FK_OK;
+}
+
 /* ----------------------------------------------------------------------- render */
 static int fk_render_any(fk_handle *h, const fk_plan *p, const void *in, void *out,
                          int n_frames, int channels, int is_f32, void *stream)
@@ -572,8 +587,9 @@ static int fk_render_any(fk_handle *h, const fk_plan *p, const void *in, void *o
     if (p->h != h) return fk_fail(h, FK_EINVAL, "plan belongs to another handle");
     if (channels != 1 && channels != 3) /* blockwise.py:160-161 */
         return fk_fail(h, FK_EINVAL, "render supports 1 or 3 channels, got %d", channels);
-    if (n_frames < 1 || n_frames > p->n_frames)
-        return fk_fail(h, FK_EINVAL, "n_frames %d outside the %d planned", n_frames, p->n_frames);
+    /* the work lists cover every planned frame: rendering fewer would write past `out` */
+    if (n_frames != p->n_frames)
+        return fk_fail(h, FK_EINVAL, "%d frames to render but %d planned", n_frames, p->n_frames);
     if (in == out) return fk_fail(h, FK_EINVAL, "render cannot run in place");
     FK_CUDA(h, cudaSetDevice(h->device));
     int launches = 0;
@@ -639,10 +655,18 @@ static int fk_foveate_host_any(fk_handle *h, const fk_params *prm, int W, int H,
         FK_CUDA(h, cudaDeviceSynchronize());
         fk_release_stage(h);
         for (int i = 0; i < fk_handle::kStreams; i++) {
-            FK_CUDA(h, cudaMalloc(&h->stage_in[i], need));
-            FK_CUDA(h, cudaMalloc(&h->stage_out[i], need));
-            int rc = fk_plan_create(h, W, H, prm->fragment_size, chunk, &h->stage_plan[i]);
-            if (rc != FK_OK) return rc;
+            cudaError_t ce = cudaMalloc(&h->stage_in[i], need);
+            if (ce == cudaSuccess) ce = cudaMalloc(&h->stage_out[i], need);
+            int rc = ce == cudaSuccess ? fk_plan_create(h, W, H, prm->fragment_size, chunk,
+                                                        &h->stage_plan[i])
+                                       : fk_cuda_fail(h, ce, "cudaMalloc(staging)");
+            if (rc != FK_OK) { /* no half-built pipeline is left behind */
+                std::string msg = h->err;
+                fk_release_stage(h);
+                h->stage_w = h->stage_h = h->stage_f = 0;
+                h->err = msg;
+                return rc;
+            }
         }
         h->stage_bytes = need;
         h->stage_w = W;
@@ -650,21 +674,33 @@ static int fk_foveate_host_any(fk_handle *h, const fk_params *prm, int W, int H,
         h->stage_f = prm->fragment_size;
         h->stage_frames = chunk;
     }
+    /* every fixation is checked before anything is queued (retinal.py:73-74), so an invalid
+     * one cannot leave earlier chunks' copies in flight */
+    for (int i = 0; i < N; i++) {
+        const double fx = fix[2 * i], fy = fix[2 * i + 1];
+        if (!(fx >= 0 && fx < W && fy >= 0 && fy < H))
+            return fk_fail(h, FK_EINVAL, "fixation (%g, %g) outside %dx%d image", fx, fy, W, H);
+    }
+    auto drain = [&](int rc) { /* an error mid-pipeline: wait for what is already queued */
+        for (int i = 0; i < fk_handle::kStreams; i++) cudaStreamSynchronize(h->streams[i]);
+        return rc;
+    };
     int idx = 0;
     for (int first = 0; first < N; first += chunk, idx++) {
         const int n = (N - first) < chunk ? (N - first) : chunk;
         const int slot = idx % fk_handle::kStreams;
         cudaStream_t s = h->streams[slot];
         const size_t off = frame_bytes * first, bytes = frame_bytes * n;
-        FK_CUDA(h, cudaMemcpyAsync(h->stage_in[slot], (const char *)in + off, bytes,
-                                   cudaMemcpyHostToDevice, s));
+        cudaError_t ce = cudaMemcpyAsync(h->stage_in[slot], (const char *)in + off, bytes,
+                                         cudaMemcpyHostToDevice, s);
+        if (ce != cudaSuccess) return drain(fk_cuda_fail(h, ce, "cudaMemcpyAsync(H2D)"));
         int rc = fk_plan_model(h->stage_plan[slot], prm, n, fix + 2 * (size_t)first, 0, s);
-        if (rc != FK_OK) return rc;
+        if (rc != FK_OK) return drain(rc);
         rc = fk_render_any(h, h->stage_plan[slot], h->stage_in[slot], h->stage_out[slot], n, C,
                            is_f32, s);
-        if (rc != FK_OK) return rc;
-        FK_CUDA(h, cudaMemcpyAsync((char *)out + off, h->stage_out[slot], bytes,
-                                   cudaMemcpyDeviceToHost, s));
+        if (rc != FK_OK) return drain(rc);
+        ce = cudaMemcpyAsync((char *)out + off, h->stage_out[slot], bytes, cudaMemcpyDeviceToHost, s);
+        if (ce != cudaSuccess) return drain(fk_cuda_fail(h, ce, "cudaMemcpyAsync(D2H)"));
     }
     for (int i = 0; i < fk_handle::kStreams; i++) FK_CUDA(h, cudaStreamSynchronize(h->streams[i]));
     return FK_OK;

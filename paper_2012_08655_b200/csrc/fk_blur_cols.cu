@@ -908,15 +908,131 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
     }
 }
 
+/*
+ * Horizontal task on float32 frames.  TMA fetches whole 16-byte quads of a row only (the
+ * global address of a box must be 16-byte aligned), and a tile starts on any float: its first
+ * float is 3 (x0 - r).  The residue is absorbed by the TAPS: the stream starts zf = (x0 - r)
+ * mod 4 pixels left of the tile, on a pixel that is a multiple of four (a float that is a
+ * multiple of 12, quad-aligned), and the filter is padded with zf zeros in front and zb at
+ * the end up to a multiple of four taps.  The block lands as raw[quad][row][4 floats] with
+ * stream float 0 at raw float 0, so a lane's stream is one LDS.128 per quad, kQStride bytes
+ * apart: no shift, no conversion.  Zero taps are never multiplied -- the image may hold
+ * anything beyond the filter's support, and a partial first / last chunk costs what its
+ * real taps cost: the first and the last chunk of a task run a copy of the chunk whose four
+ * tap groups are guarded (uniform branches), the chunks in between the plain one.
+ * `row_s` is the shared address of the lane's row inside the first quad of the warp's
+ * columns, `wts` of the padded taps, nchunk = (zf + L + zb) / 4.
+ */
+__device__ __forceinline__ void h_float(uint32_t row_s, uint32_t wts, int nchunk, int zf, int zb,
+                                        float (&acc)[kSegF])
+{
+    constexpr int C = kC, NW = 16 * C;
+    float win[NW];
+#pragma unroll
+    for (int v = 0; v < 3 * C; v++) {
+        const float4 x = lds128(row_s + (uint32_t)(v * kQStride));
+        win[4 * v + 0] = x.x;
+        win[4 * v + 1] = x.y;
+        win[4 * v + 2] = x.z;
+        win[4 * v + 3] = x.w;
+    }
+#pragma unroll
+    for (int j = 0; j < kSegF; j++) acc[j] = 0.0f;
+    uint32_t nxt = row_s + 3 * C * kQStride;
+    float4 g4 = lds128(wts);
+    uint32_t wa = wts + 16;
+    auto refill = [&](const int p) { /* ring slot p + 3 <- the next three quads of the row */
+#pragma unroll
+        for (int v = 0; v < C; v++) {
+            const float4 x = lds128(nxt + (uint32_t)(v * kQStride));
+            const int q = (((p + 3) % 4) * C + v) * 4;
+            win[q + 0] = x.x;
+            win[q + 1] = x.y;
+            win[q + 2] = x.z;
+            win[q + 3] = x.w;
+        }
+        nxt += C * kQStride;
+    };
+    auto chunk = [&](const int p) {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa); /* next chunk's taps (one padding quad follows the last) */
+        wa += 16;
+        refill(p);
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+#pragma unroll
+            for (int j = 0; j < kSegF; j++)
+                acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
+        }
+    };
+    auto guarded = [&](const int p, const int tlo, const int thi) { /* taps [tlo, thi) only */
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        g4 = lds128(wa);
+        wa += 16;
+        refill(p);
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            if (t >= tlo && t < thi) {
+#pragma unroll
+                for (int j = 0; j < kSegF; j++)
+                    acc[j] = fmaf(g[t], win[(p * 4 * C + C * t + j) % NW], acc[j]);
+            }
+        }
+    };
+    guarded(0, zf, nchunk == 1 ? 4 - zb : 4);
+    if (nchunk == 1) return;
+    const int nmid = nchunk - 1; /* chunks [1, nmid) are whole */
+    for (int c = 1; c < nmid; c += 4) {
+        chunk(1);
+        if (c + 1 >= nmid) break;
+        chunk(2);
+        if (c + 2 >= nmid) break;
+        chunk(3);
+        if (c + 3 >= nmid) break;
+        chunk(0);
+    }
+    switch (nmid & 3) { /* the last chunk, at the phase the ring has reached */
+    case 0: guarded(0, 0, 4 - zb); break;
+    case 1: guarded(1, 0, 4 - zb); break;
+    case 2: guarded(2, 0, 4 - zb); break;
+    default: guarded(3, 0, 4 - zb); break;
+    }
+}
+
+/*
+ * float32 frames, items at the left / right image border: clamp-to-edge in x
+ * (blockwise.py:147).  TMA fills the quads outside the row with zeros; the stream floats
+ * left and right of the image, which repeat the edge pixel, are fetched from global memory
+ * here.  Four threads per box row; `e0` is the image float of stream float 0 (a multiple of
+ * 3, so the channel of stream float j is j mod 3), `n` the stream floats that meet taps.
+ */
+__device__ __noinline__ void patch_x_edges_f32(unsigned char *raw, const float *__restrict__ src,
+                                               int e0, int n, int WC, int ys_c, int H, int tid)
+{
+    const int row = tid >> 2;
+    const int gy = ys_c + row < H - 1 ? ys_c + row : H - 1;
+    const float *grow = src + (size_t)gy * WC;
+    float *rrow = reinterpret_cast<float *>(raw + row * kQB);
+    auto put = [&](int j, int gi) { rrow[(j >> 2) * (kQStride / 4) + (j & 3)] = __ldg(grow + gi); };
+    const int nl = e0 < 0 ? (-e0 < n ? -e0 : n) : 0;
+#pragma unroll 1
+    for (int j = tid & 3; j < nl; j += 4) put(j, j % kC);
+    int j0 = WC - e0;
+    j0 = j0 < nl ? nl : j0;
+#pragma unroll 1
+    for (int j = j0 + (tid & 3); j < n; j += 4) put(j, WC - kC + j % kC);
+}
+
 /* Three resident CTAs per SM with 167 registers beat four with 127 (27.0 k against 26.8 k
  * frames/s on the bench, 19.4 k against 18.8 k with corner fixations): at 127 the compiler
  * rematerialises addresses and constants inside the task set-up. */
-__global__ void __launch_bounds__(kThreads, 3)
-fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t *__restrict__ out,
-              int klass, int wts_floats, int nq, int icap, int ipitch, int nbuf)
+template <typename T, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *__restrict__ in,
+            T *__restrict__ out, int klass, int wts_floats, int nq, int icap, int ipitch, int nbuf)
 {
     constexpr int C = kC;
-    typedef uint8_t T;
+    constexpr bool kBytes = sizeof(T) == 1;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     /* layout: [raw x nbuf: nq chunks x 32 rows x 16 B][barriers + item slots, 128 B][per-warp taps x 3][ring]
      * nbuf = 2 where a second raw buffer does not cost a resident CTA: the TMA request then
@@ -946,11 +1062,16 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
      * (possibly left of the image: TMA fills what is outside with zeros) and at the first
      * source row clamped into the image. */
     auto issue = [&](const item_geo &g, int rb, int buf) {
-        /* the H pass's stream starts 3 zpad bytes left of the tile (front-padded taps) */
-        const int byte0 = (g.x0 - g.r) * C - C * (4 * g.nchunk - g.L);
+        /* the H pass's stream starts left of the tile (front-padded taps): uint8 -- 3 zpad
+         * bytes, fetched from the 16-byte chunk that holds the stream's first byte; float32
+         * -- on the pixel at or below the tile's first that is a multiple of four, whose first
+         * float starts a quad (h_float) */
+        const int e0 = kBytes ? (g.x0 - g.r) * C - C * (4 * g.nchunk - g.L)
+                              : ((g.x0 - g.r) & ~3) * C;
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
         mbar_expect_tx(bar + buf, (uint32_t)raw_bytes);
-        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, byte0 >> 4, g.f);
+        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, kBytes ? e0 >> 4 : e0 >> 2,
+                    g.f);
     };
     auto fill_taps = [&](const uint4 q, int slot) {
         const int L = (int)((q.z >> 8) & 0x1fffu);
@@ -1024,13 +1145,24 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
             d_pending = true;
         }
         const float *w_cur = wts + (warp * 3 + wslot) * wts_floats; /* taps, V pass */
-        float *w_h = wts + (warp * 3 + 2) * wts_floats;             /* scaled copy, H pass */
+        /* H pass: its own copy -- scaled by 2^120 for uint8 frames (bytes_to_float4_s);
+         * padded with zf zeros in front for float32 frames (h_float) */
+        float *w_h = wts + (warp * 3 + 2) * wts_floats;
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
         {
             const int L = (int)((q_cur.z >> 8) & 0x1fffu);
-            const int n = 4 * ((L + 3) >> 2) + 4;
-            for (int i = lane; i < n; i += 32) w_h[i] = w_cur[i] * kTapScaleH;
+            const int zv = 4 * ((L + 3) >> 2) - L; /* zeros in front of w_cur */
+            if (kBytes) {
+                const int n = L + zv + 4;
+                for (int i = lane; i < n; i += 32) w_h[i] = w_cur[i] * kTapScaleH;
+            } else {
+                const int xr = (int)(q_cur.y & 0xffffu) - ((L - 1) >> 1);
+                const int z = xr & 3;
+                const int n = 4 * ((z + L + 3) >> 2) + 4;
+                for (int i = lane; i < n; i += 32)
+                    w_h[i] = i >= z && i < z + L ? w_cur[i - z + zv] : 0.0f;
+            }
             __syncwarp();
         }
 
@@ -1039,7 +1171,10 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
         const int nchunk = g.nchunk, th = g.th, tw = g.tw;
         const int zpad = 4 * nchunk - g.L; /* zeros in front of the taps: 3 or 1 */
         T *dst = out + (size_t)g.f * H * W * C;
-        const int skew_h = ((x0 - r) * C - C * zpad) & 15;         /* the stream's byte 0 in the box */
+        const int zf = kBytes ? zpad : (x0 - r) & 3;               /* zero taps in front, H pass */
+        const int e0 = (x0 - r - zf) * C;                          /* image element of stream element 0 */
+        const int skew_h = kBytes ? e0 & 15 : 0;                   /* the stream's element 0 in the box */
+        const int nchunk_h = (zf + g.L + 3) >> 2;
         const int skew = skew_h + C * zpad;                        /* tile float 0 = raw byte skew */
         const int nl = r - x0 > 0 ? r - x0 : 0;                    /* tile pixels left of the image */
         const int nr = x0 + fw + r - W > 0 ? x0 + fw + r - W : 0; /* ... and right of it */
@@ -1067,7 +1202,13 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
                 }
                 if (have_next) fill_taps(q_nxt, wslot ^ 1);
             }
-            if (nl | nr) {
+            if (!kBytes) {
+                if (e0 < 0 || e0 + tw + C * zf > W * C) {
+                    patch_x_edges_f32(raw, reinterpret_cast<const float *>(in) + (size_t)g.f * H * W * C,
+                                      e0, tw + C * zf, W * C, ys_c, H, tid);
+                    __syncthreads();
+                }
+            } else if (nl | nr) {
                 /* clamp-to-edge in x (blockwise.py:147): the raw bytes left and right of the
                  * image become copies of the edge pixel.  Four lanes per box row, each one
                  * 16-byte chunk at a time: the run is periodic in 3 bytes, so a chunk is four of
@@ -1113,8 +1254,12 @@ fk_blur_bytes(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, uint8_t 
             if (active && lane < nrows) {
                 float hacc[kSegF];
                 const int brow = fast_clamp(ys + lane, 0, H - 1) - ys_c; /* box row */
-                h_bytes(raw_s + (uint32_t)(brow * kQB), skew_h + kSegF * warp, smem_u32(w_h), nchunk,
-                        zpad, hacc);
+                if (kBytes)
+                    h_bytes(raw_s + (uint32_t)(brow * kQB), skew_h + kSegF * warp, smem_u32(w_h),
+                            nchunk, zpad, hacc);
+                else
+                    h_float(raw_s + (uint32_t)(brow * kQB + (kSegF / 4) * warp * kQStride),
+                            smem_u32(w_h), nchunk_h, zf, 4 * nchunk_h - zf - g.L, hacc);
                 int rr = rbm + lane + zpad; /* zpad rows down: see v_task_px */
                 rr = rr >= icap ? rr - icap : rr;
                 float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
@@ -1250,7 +1395,7 @@ cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     return cudaGetLastError();
 }
 
-/* The batch as (16 bytes, rows, 16-byte chunks of a row, frames) with boxes of
+/* uint8: the batch as (16 bytes, rows, 16-byte chunks of a row, frames) with boxes of
  * 16 B x 32 rows x nq chunks: lands as [chunk][row][16 B] in shared memory. */
 bool make_tensor_map_chunks(CUtensorMap *map, const void *in, int W, int H, int n_frames, int nq)
 {
@@ -1267,14 +1412,39 @@ bool make_tensor_map_chunks(CUtensorMap *map, const void *in, int W, int H, int 
     return r == CUDA_SUCCESS;
 }
 
-cudaError_t launch_bytes(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in, void *out,
-                         int n_frames, int class_length, cudaStream_t s, bool *taken)
+/* float32: the batch as (4 floats, rows, quads of a row, frames) with boxes of
+ * 4 floats x 32 rows x nq quads: lands as [quad][row][4 floats] in shared memory. */
+bool make_tensor_map_quads(CUtensorMap *map, const void *in, int W, int H, int n_frames, int nq)
+{
+    encode_tiled_fn enc = get_encode_tiled();
+    const size_t rowf = (size_t)W * kC;
+    if (!enc || ((uintptr_t)in & 15) != 0 || (rowf & 3) != 0 || nq > 256) return false;
+    const size_t pitch = rowf * sizeof(float);
+    cuuint64_t dims[4] = {4, (cuuint64_t)H, (cuuint64_t)(rowf / 4), (cuuint64_t)n_frames};
+    cuuint64_t strides[3] = {(cuuint64_t)pitch, (cuuint64_t)kQB, (cuuint64_t)pitch * H};
+    cuuint32_t box[4] = {4, (cuuint32_t)kTB, (cuuint32_t)nq, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void *>(in), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <typename T>
+cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in, void *out,
+                       int n_frames, int class_length, cudaStream_t s, bool *taken)
 {
     *taken = false;
+    constexpr bool bytes = sizeof(T) == 1;
     const int nchunk = (class_length + 3) / 4;
     const int r = (class_length - 1) / 2;
-    const int wts_floats = 4 * nchunk + 4;
-    const int nq = (168 + 6 * r + kQB - 1) / kQB; /* chunks a lane's word stream can reach */
+    /* float32: up to three more zeros in front of the H pass's taps (h_float) */
+    const int nchunk_h = bytes ? nchunk : (class_length + 6) / 4;
+    const int wts_floats = 4 * nchunk_h + 4;
+    /* chunks / quads a lane's stream can reach: uint8 -- 15 bytes of skew + 96 + 12 per chunk
+     * of taps + what the window loads ahead; float32 -- the last warp starts at quad 18 and
+     * reads 9 + 3 per chunk of taps */
+    const int nq = bytes ? (168 + 6 * r + kQB - 1) / kQB : 18 + 9 + 3 * nchunk_h;
     const int icap = (2 * r + kTB + 3) & ~3;
     const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
     size_t smem = (size_t)nq * kQStride + 128 +
@@ -1282,8 +1452,15 @@ cudaError_t launch_bytes(fk_handle *h, const fk_plan_dev &pd, int klass, const v
     if (smem > h->prop.sharedMemPerBlockOptin) return cudaSuccess;
     CUtensorMap map;
     memset(&map, 0, sizeof map);
-    if (!make_tensor_map_chunks(&map, in, pd.width, pd.height, n_frames, nq)) return cudaSuccess;
-    auto kernel = fk_blur_bytes;
+    if (bytes ? !make_tensor_map_chunks(&map, in, pd.width, pd.height, n_frames, nq)
+              : !make_tensor_map_quads(&map, in, pd.width, pd.height, n_frames, nq))
+        return cudaSuccess;
+    /* Layouts that fit three times on an SM run with the register budget of three resident
+     * CTAs, the others with that of two. */
+    const size_t per_sm = h->prop.sharedMemPerMultiprocessor;
+    const size_t reserved = h->prop.reservedSharedMemPerBlock;
+    const bool two = 3 * (smem + reserved) > per_sm;
+    auto kernel = two ? fk_blur_tma<T, 2> : fk_blur_tma<T, 3>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -1305,8 +1482,8 @@ cudaError_t launch_bytes(fk_handle *h, const fk_plan_dev &pd, int klass, const v
         }
     }
     const int grid = h->prop.multiProcessorCount * occ;
-    kernel<<<grid, kThreads, smem, s>>>(map, pd, (uint8_t *)out, klass, wts_floats, nq, icap, ipitch,
-                                        nbuf);
+    kernel<<<grid, kThreads, smem, s>>>(map, pd, (const T *)in, (T *)out, klass, wts_floats, nq,
+                                        icap, ipitch, nbuf);
     *taken = true;
     return cudaGetLastError();
 }
@@ -1322,12 +1499,20 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
 {
     CUtensorMap map;
     memset(&map, 0, sizeof map);
-    if (is_f32) return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
+    if (is_f32) {
+        /* float32 by TMA: fk_blur_tma<float>, the H pass reads the landed floats directly
+         * (variants 2 and 4: plain-load staging through fk_blur_cols) */
+        if (h->variant != 2 && h->variant != 4) {
+            cudaError_t e = launch_tma<float>(h, pd, klass, in, out, n_frames, class_length, s, taken);
+            if (e != cudaSuccess || *taken) return e;
+        }
+        return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
+    }
     /* uint8 by TMA: fk_blur_bytes, the kernel whose H pass reads the TMA bytes directly -- no
      * working tile, no conversion pass, no CTA barrier, 3 CTAs per SM up to 105 taps.  (Until the taps were padded in front it only won for the long filters.)
      * Variant 4: fk_blur_cols for every class, variant 5: same as the default. */
     if (h->variant == 5 || h->variant == 0 || h->variant == 6) { /* 6: one raw buffer (A/B runs) */
-        cudaError_t e = launch_bytes(h, pd, klass, in, out, n_frames, class_length, s, taken);
+        cudaError_t e = launch_tma<uint8_t>(h, pd, klass, in, out, n_frames, class_length, s, taken);
         if (e != cudaSuccess || *taken) return e;
     }
     const bool tma = h->variant != 2 && make_tensor_map(&map, in, pd.width, pd.height, kC, n_frames);

@@ -50,6 +50,8 @@ enum {
 #define FK_CLASS_L4 127
 #define FK_CLASS_GENERIC 5
 #define FK_CLASS_COPY 6
+#define FK_COUNTER_WORDS (2 * FK_NCLASS + 1)
+#define FK_COUNTER_BAD (2 * FK_NCLASS)
 
 static __host__ __device__ __forceinline__ int fk_class_of(int L)
 {
@@ -91,7 +93,8 @@ struct fk_plan_dev {
     int strip_rows;      /* tallest strip the plan kernel merges fragments into (fk_strip_rows_for) */
     size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */
     fk_item *items;      /* [FK_NCLASS][items_cap] */
-    int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors */
+    int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors;
+                            [2 NCLASS]: frames whose fixation lies outside the image */
     double *sigma;       /* [frames][cap] */
     int32_t *raw_length; /* [frames][cap] */
     int32_t *length;     /* [frames][cap], foveal cell forced to 1 */

@@ -216,7 +216,32 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
 
     /* retinal.py:73: fixation must satisfy 0 <= fx < w and 0 <= fy < h (NaN fails) */
     if (!(fx >= 0.0 && fx < (double)W && fy >= 0.0 && fy < (double)H)) {
+        /* the host raises ValueError (fk_plan_status); the frame is copied through so that
+         * the output buffer is defined whatever the caller does with the error */
         if (tid < FK_META_WORDS) meta[tid] = tid == FK_META_STATUS ? 1 : 0;
+        const int ncx = (W + 254) / 255, ncy = (H + 2046) / 2047;
+        if (ncx * ncy <= pd.cap) {
+            __shared__ int s_base;
+            if (tid == 0) {
+                atomicAdd(&pd.counters[FK_COUNTER_BAD], 1);
+                s_base = atomicAdd(&pd.counters[FK_CLASS_COPY], ncx * ncy);
+            }
+            __syncthreads();
+            fk_item *dst = pd.items + (size_t)FK_CLASS_COPY * pd.items_cap + s_base;
+            for (int i = tid; i < ncx * ncy; i += blockDim.x) {
+                const int cy = i / ncx, cx = i - cy * ncx;
+                const int x0 = cx * 255, y0 = cy * 2047;
+                const int fw = W - x0 < 255 ? W - x0 : 255, fh = H - y0 < 2047 ? H - y0 : 2047;
+                fk_item it;
+                it.frame = (uint32_t)f;
+                it.xy = (uint32_t)x0 | ((uint32_t)y0 << 16);
+                it.geom = (uint32_t)fw | (1u << 8) | ((uint32_t)fh << 21);
+                it.taps_off = 0;
+                dst[i] = it;
+            }
+        } else if (tid == 0) {
+            atomicAdd(&pd.counters[FK_COUNTER_BAD], 1);
+        }
         return;
     }
     const long long ifx = (long long)floor(fx), ify = (long long)floor(fy);

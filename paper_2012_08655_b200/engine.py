@@ -49,6 +49,7 @@ class DevicePlan:
         self.fragment_size = int(fragment_size)
         self.max_frames = int(max_frames)
         self.n_frames = 0
+        self.fix_on_device = False
         ptr = C.c_void_p()
         check(engine._lib.fk_plan_create(engine._h, self.size[0], self.size[1],
                                          self.fragment_size, self.max_frames, C.byref(ptr)),
@@ -79,9 +80,11 @@ class DevicePlan:
         else:
             fix = np.ascontiguousarray(np.asarray(fixations, dtype=np.float64).reshape(-1, 2))
             n, ptr, on_dev = fix.shape[0], _np_ptr(fix), 0
-        check(eng._lib.fk_plan_model(self._p, C.byref(prm), n, ptr, on_dev,
-                                     eng._stream(stream)), eng._h)
+        with eng._lock:
+            check(eng._lib.fk_plan_model(self._p, C.byref(prm), n, ptr, on_dev,
+                                         eng._stream(stream)), eng._h)
         self.n_frames = n
+        self.fix_on_device = bool(on_dev)
         return self
 
     def density(self, density_map, sigma_max, fragment_size, fixations, use_shift=True,
@@ -96,10 +99,13 @@ class DevicePlan:
             mode, (sx, sy) = 2, (int(shift[0]), int(shift[1]))
         prm = FkParams(fragment_size=int(fragment_size), use_shift=mode, shift_x=sx, shift_y=sy)
         fix = np.ascontiguousarray(np.asarray(fixations, dtype=np.float64).reshape(-1, 2))
-        check(eng._lib.fk_plan_density(self._p, C.byref(prm), fix.shape[0], _np_ptr(fix), 0,
-                                       _np_ptr(dm), dm.shape[1], dm.shape[0],
-                                       C.c_double(float(sigma_max)), eng._stream(stream)), eng._h)
+        with eng._lock:
+            check(eng._lib.fk_plan_density(self._p, C.byref(prm), fix.shape[0], _np_ptr(fix), 0,
+                                           _np_ptr(dm), dm.shape[1], dm.shape[0],
+                                           C.c_double(float(sigma_max)), eng._stream(stream)),
+                  eng._h)
         self.n_frames = fix.shape[0]
+        self.fix_on_device = False
         return self
 
     def set_grid(self, shift, lengths, offsets, coeffs, stream=None):
@@ -109,11 +115,22 @@ class DevicePlan:
         offsets = np.ascontiguousarray(offsets, dtype=np.int32)
         coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
         gh, gw = lengths.shape
-        check(eng._lib.fk_plan_set_grid(self._p, int(shift[0]), int(shift[1]), gw, gh,
-                                        _np_ptr(lengths), _np_ptr(offsets), _np_ptr(coeffs),
-                                        int(coeffs.size), eng._stream(stream)), eng._h)
+        with eng._lock:
+            check(eng._lib.fk_plan_set_grid(self._p, int(shift[0]), int(shift[1]), gw, gh,
+                                            _np_ptr(lengths), _np_ptr(offsets), _np_ptr(coeffs),
+                                            int(coeffs.size), eng._stream(stream)), eng._h)
         self.n_frames = 1
+        self.fix_on_device = False
         return self
+
+    def bad_fixations(self, stream=None) -> int:
+        """Frames of the last plan whose fixation was outside the image (fk_plan_status;
+        synchronises).  Host fixations never get that far: fk_plan_model rejects them."""
+        eng = self.engine
+        bad = C.c_int(0)
+        with eng._lock:
+            check(eng._lib.fk_plan_status(self._p, C.byref(bad), eng._stream(stream)), eng._h)
+        return int(bad.value)
 
     def read(self, frame=0, stream=None) -> dict:
         """Synchronising read-back of one frame's plan."""
@@ -123,8 +140,9 @@ class DevicePlan:
         length = np.empty(self.cap, np.int32)
         view = FkPlanView(sigma=sigma.ctypes.data, raw_length=raw.ctypes.data,
                           length=length.ctypes.data)
-        check(eng._lib.fk_plan_read(self._p, int(frame), C.byref(view), eng._stream(stream)),
-              eng._h)
+        with eng._lock:
+            check(eng._lib.fk_plan_read(self._p, int(frame), C.byref(view), eng._stream(stream)),
+                  eng._h)
         if view.status != 0:
             raise ValueError("fixation outside image")
         gw, gh = view.grid_w, view.grid_h
@@ -141,8 +159,9 @@ class DevicePlan:
         count = self.n_frames - first if count is None else count
         lengths = np.empty((count, self.cap), np.int32)
         meta = np.empty((count, META_WORDS), np.int32)
-        check(eng._lib.fk_plan_read_lengths(self._p, int(first), int(count), _np_ptr(lengths),
-                                            _np_ptr(meta), eng._stream(stream)), eng._h)
+        with eng._lock:
+            check(eng._lib.fk_plan_read_lengths(self._p, int(first), int(count), _np_ptr(lengths),
+                                                _np_ptr(meta), eng._stream(stream)), eng._h)
         return lengths, meta
 
 
@@ -220,6 +239,8 @@ class Engine:
         n, h, w, c = frames.shape
         if (w, h) != plan.size:
             raise ValueError(f"grid does not match image {(w, h)}")
+        if n != plan.n_frames:
+            raise ValueError(f"{n} frames but {plan.n_frames} fixations planned")
         if out is None:
             out = torch.empty_like(frames)
         elif out.shape != frames.shape or out.dtype != frames.dtype or not out.is_contiguous() \
@@ -237,13 +258,27 @@ class Engine:
         return out
 
     def foveate_device(self, frames: torch.Tensor, fixations, params, use_shift=True,
-                       out=None, stream=None):
-        """plan + render for frames already resident on this GPU; returns (out, plan)."""
+                       out=None, stream=None, validate=True):
+        """plan + render for frames already resident on this GPU; returns (out, plan).
+
+        Fixations that live on the device cannot be range-checked on the host; with
+        ``validate`` (default) the plan kernel's count of out-of-image fixations is read
+        back after the render has been queued (one 4-byte copy, synchronises the stream)
+        and ValueError is raised as the reference does (retinal.py:73-74).  Pass
+        ``validate=False`` to keep the call asynchronous: such frames are then copied
+        through unchanged."""
         n, h, w, _ = frames.shape
+        nfix = fixations.shape[0] if hasattr(fixations, "shape") else len(fixations)
+        if nfix != n:
+            raise ValueError(f"{n} frames but {nfix} fixations")
         with self._lock:
             plan = self.plan_for((w, h), params.fragment_size, n)
             plan.model(params, fixations, use_shift=use_shift, stream=stream)
             out = self.render(frames, plan, out=out, stream=stream)
+            if validate and plan.fix_on_device:
+                bad = plan.bad_fixations(stream=stream)
+                if bad:
+                    raise ValueError(f"fixation of {bad} frame(s) outside {w}x{h} image")
         return out, plan
 
     def foveate_host(self, frames: np.ndarray, fixations: np.ndarray, params, out=None,
