@@ -149,6 +149,18 @@ int fk_plan_read(fk_plan *p, int frame, fk_plan_view *out, void *stream);
 int fk_plan_read_lengths(fk_plan *p, int first, int count, int32_t *lengths_host,
                          int32_t *meta_host, void *stream);
 
+/* The render kernels' work lists of the last plan, for accounting (bench.py reports the FLOPs
+ * the merged strips execute next to the algorithmic count of costs.py).  A plan holds
+ * fk_plan_item_classes() lists by tap count (the last one: identity fragments, plain copies);
+ * an item is four uint32: frame, x0 | y0 << 16, width | taps << 8 | height << 21, tap offset --
+ * a rectangle at most 32 pixels wide of vertically adjacent fragments that share one filter
+ * (merging them is exact: an output pixel depends only on the image and its filter,
+ * blockwise.py:136-153).  *count receives the list's length; up to `capacity` items are
+ * copied to items_host (may be NULL to query the length).  Synchronises the stream. */
+int fk_plan_item_classes(void);
+int fk_plan_read_items(fk_plan *p, int klass, uint32_t *items_host, int capacity, int *count,
+                       void *stream);
+
 /* Frames of the last fk_plan_model / fk_plan_density call whose fixation lies outside the
  * image or is not a number (retinal.py:73-74 raises ValueError("fixation ... outside image")).
  * Host fixations are rejected before anything is launched; fixations that are already on

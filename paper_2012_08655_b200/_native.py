@@ -21,7 +21,7 @@ EXPORTS = [
     "fk_get_device_info", "fk_build_lut", "fk_lut_max_length", "fk_lut_read",
     "fk_plan_create", "fk_plan_destroy", "fk_plan_cell_capacity", "fk_plan_model",
     "fk_plan_density", "fk_plan_set_grid", "fk_plan_read", "fk_plan_read_lengths",
-    "fk_plan_status", "fk_render_u8",
+    "fk_plan_status", "fk_plan_item_classes", "fk_plan_read_items", "fk_render_u8",
     "fk_render_f32", "fk_set_kernel_variant", "fk_launch_count", "fk_foveate_host_u8",
     "fk_foveate_host_f32", "fk_host_alloc", "fk_host_free", "fk_measure_fp32_peak", "fk_ssim_u8", "fk_ssim_stats",
 ]
@@ -80,6 +80,8 @@ def _declare(lib):
         "fk_plan_read": (i32, [vp, i32, P(FkPlanView), vp]),
         "fk_plan_read_lengths": (i32, [vp, i32, i32, vp, vp, vp]),
         "fk_plan_status": (i32, [vp, P(C.c_int), vp]),
+        "fk_plan_item_classes": (i32, []),
+        "fk_plan_read_items": (i32, [vp, i32, vp, i32, P(C.c_int), vp]),
         "fk_render_u8": (i32, [vp, vp, vp, vp, i32, i32, vp]),
         "fk_render_f32": (i32, [vp, vp, vp, vp, i32, i32, vp]),
         "fk_set_kernel_variant": (i32, [vp, i32]),

@@ -26,14 +26,46 @@ def frame_macs(size, fragment_size: int, shift, lengths) -> int:
 
 def batch_flops(size, fragment_size: int, channels: int, lengths, meta) -> float:
     """Total algorithmic FLOPs (2 per MAC, all channels) of a planned batch, from
-    DevicePlan.read_lengths() output."""
+    DevicePlan.read_lengths() output.  Frames that share a tiling shift share their fragment
+    sizes, so the batch is summed shift by shift (at most fragment_size^2 groups)."""
+    w, h = size
+    meta = np.asarray(meta)
+    lengths = np.asarray(lengths)
+    key = meta[:, 0].astype(np.int64) * 65536 + meta[:, 1]
     total = 0
-    for i in range(len(meta)):
-        sx, sy, gw, gh = (int(v) for v in meta[i, :4])
-        total += frame_macs(size, fragment_size, (sx, sy), lengths[i, : gw * gh])
+    for k in np.unique(key):
+        rows = np.nonzero(key == k)[0]
+        sx, sy, gw, gh = (int(v) for v in meta[rows[0], :4])
+        spx = fragment_spans(w, fragment_size, sx)
+        spy = fragment_spans(h, fragment_size, sy)
+        fw = (spx[:, 1] - spx[:, 0])[None, None, :]
+        fh = (spy[:, 1] - spy[:, 0])[None, :, None]
+        L = lengths[rows, : gw * gh].astype(np.int64).reshape(len(rows), gh, gw)
+        r = (L - 1) // 2
+        total += int(np.where(L > 1, L * (fw * (fh + 2 * r) + fw * fh), 0).sum())
     return 2.0 * channels * total
 
 
 def frame_bytes(size, channels: int, itemsize: int) -> int:
     """Algorithmic HBM bytes per frame: every sample read once and written once."""
     return 2 * size[0] * size[1] * channels * itemsize
+
+
+def items_macs(items) -> int:
+    """Per-channel multiply-accumulates the render kernels execute for one work list
+    (DevicePlan.read_items): L * (w * (h + 2r) + w * h) per strip.  Merged strips run the
+    horizontal pass over the 2r halo rows between their fragments once, so this is below
+    the algorithmic count of frame_macs, which charges every fragment its own halo."""
+    it = np.asarray(items, dtype=np.int64).reshape(-1, 4)
+    if it.size == 0:
+        return 0
+    w = it[:, 2] & 0xFF
+    L = (it[:, 2] >> 8) & 0x1FFF
+    h = it[:, 2] >> 21
+    r = (L - 1) // 2
+    return int(np.where(L > 1, L * (w * (h + 2 * r) + w * h), 0).sum())
+
+
+def executed_flops(item_lists, channels: int) -> float:
+    """FLOPs the strips of a planned batch execute (2 per MAC, all channels)."""
+    return 2.0 * channels * sum(items_macs(it) for it in item_lists)

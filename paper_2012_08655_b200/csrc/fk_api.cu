@@ -564,6 +564,28 @@ int fk_plan_read(fk_plan *p, int frame, fk_plan_view *out, void *stream)
     return FK_OK;
 }
 
+int fk_plan_item_classes(void) { return FK_NCLASS; }
+
+int fk_plan_read_items(fk_plan *p, int klass, uint32_t *items_host, int capacity, int *count,
+                       void *stream)
+{
+    if (!p || !count) return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");
+    fk_handle *h = p->h;
+    if (klass < 0 || klass >= FK_NCLASS)
+        return fk_fail(h, FK_EINVAL, "class %d outside [0, %d)", klass, FK_NCLASS);
+    FK_CUDA(h, cudaSetDevice(h->device));
+    FK_CUDA(h, cudaStreamSynchronize(as_stream(stream)));
+    int32_t n = 0;
+    FK_CUDA(h, cudaMemcpy(&n, p->d.counters + klass, sizeof n, cudaMemcpyDeviceToHost));
+    *count = n;
+    if (!items_host || capacity <= 0) return FK_OK;
+    const int take = n < capacity ? n : capacity;
+    if (take > 0)
+        FK_CUDA(h, cudaMemcpy(items_host, p->d.items + (size_t)klass * p->d.items_cap,
+                              (size_t)take * sizeof(fk_item), cudaMemcpyDeviceToHost));
+    return FK_OK;
+}
+
 int fk_plan_status(fk_plan *p, int *bad_frames, void *stream)
 {
     if (!p || !bad_frames) return fk_fail(p ? p->h : nullptr, FK_EINVAL, "NULL argument");

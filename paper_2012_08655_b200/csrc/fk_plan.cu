@@ -63,8 +63,9 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  *   down    a vertical run of equal units (same cells, same taps) is cut from its top into
  *           strips of at most pd.strip_rows / F grid rows, which lets the fragments of a
  *           strip share the horizontal pass over the 2r halo rows between them.
- * Wider fragments are cut into columns FK_RECT wide (and pieces FK_STRIP_ROWS tall) without
- * merging across cells.
+ * Wider fragments are cut into columns FK_RECT wide; those merge down the grid in the same
+ * way (a 64-pixel fragment is two columns, each the head of its own strips), and only
+ * fragments taller than FK_STRIP_ROWS are cut into pieces without merging.
  */
 __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
 {
@@ -77,11 +78,12 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     const int sx = meta[FK_META_SX], sy = meta[FK_META_SY];
     const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
     const int F = pd.fragment;
-    const bool merge = F <= FK_RECT;
-    const int maxc = merge ? (pd.strip_rows / F > 1 ? pd.strip_rows / F : 1) : 1;
+    const bool merge = F <= FK_RECT;      /* cells of a grid row may merge across */
+    const bool vmerge = pd.nsub_y == 1;   /* ... and units down the grid (always, today) */
+    const int maxc = vmerge ? (pd.strip_rows / F > 1 ? pd.strip_rows / F : 1) : 1;
     const int mgrp = merge ? FK_RECT / F : 1; /* cells per horizontal unit */
     const int lead = sx > 0 ? 1 : 0;
-    const int per_cell = merge ? 1 : pd.nsub_x * pd.nsub_y;
+    const int per_cell = pd.nsub_x * pd.nsub_y; /* FK_RECT-wide columns of a wider fragment */
     if (tid < FK_NCLASS) ccount[tid] = 0;
     __syncthreads();
 
@@ -111,7 +113,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
             const int c = gy * gw + gx;
             int u0 = gx, u1 = gx + 1;
             const int L = len[c], o = off[c];
-            const bool mergeable = merge && L != 1;
+            const bool mergeable = vmerge && L != 1;
             if (mergeable) unit_of(gy, gx, u0, u1);
             if (gx != u0) { /* inside a unit headed by the cell to its left */
                 strip[c] = 0;

@@ -123,6 +123,24 @@ class DevicePlan:
         self.fix_on_device = False
         return self
 
+    def read_items(self, stream=None) -> list:
+        """The render kernels' work lists of the last plan (fk_plan_read_items): one uint32
+        [n, 4] array per tap-count class -- frame, x0 | y0 << 16, width | taps << 8 |
+        height << 21, tap offset.  For accounting (costs.items_macs); synchronises."""
+        eng = self.engine
+        out = []
+        with eng._lock:
+            for k in range(eng._lib.fk_plan_item_classes()):
+                n = C.c_int(0)
+                check(eng._lib.fk_plan_read_items(self._p, k, None, 0, C.byref(n),
+                                                  eng._stream(stream)), eng._h)
+                items = np.empty((max(n.value, 0), 4), np.uint32)
+                if n.value > 0:
+                    check(eng._lib.fk_plan_read_items(self._p, k, _np_ptr(items), n.value,
+                                                      C.byref(n), eng._stream(stream)), eng._h)
+                out.append(items)
+        return out
+
     def bad_fixations(self, stream=None) -> int:
         """Frames of the last plan whose fixation was outside the image (fk_plan_status;
         synchronises).  Host fixations never get that far: fk_plan_model rejects them."""

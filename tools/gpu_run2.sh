@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest2.log 2>&1; tail -3 gpurun_out/pytest2.log
+timeout 900 python bench.py > gpurun_out/bench2.json 2> gpurun_out/bench2.err; tail -3 gpurun_out/bench2.err
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench2.json').read().strip().splitlines()[-1])
+print('headline', round(d['value']), round(d['roofline']['frac'],3), 'exec/alg', round(d['roofline']['executed_over_algorithmic'],3), 'e2e', round(d['e2e']['value']), d['clocks'])
+for e in d['configs'] or []:
+    print(e['name'], round(e['value']), 'frac', round(e['roofline']['frac'],3), 'exec/alg', round(e['roofline']['executed_over_algorithmic'],3), 'ms', round(e['kernel_ms'],3), e['clocks'].get('sm_mhz'), e.get('e2e_value'))
+PY
