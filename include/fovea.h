@@ -178,13 +178,16 @@ int fk_render_u8(fk_handle *h, const fk_plan *p, const uint8_t *in_dev, uint8_t 
 int fk_render_f32(fk_handle *h, const fk_plan *p, const float *in_dev, float *out_dev,
                   int n_frames, int channels, void *stream);
 
-/* Kernel selection for tests and profiling.  0 = default (RGB uint8 by TMA: fk_blur_bytes;
- * other RGB frames: fk_blur_cols; gray: fk_blur_fast; generic kernel where none of them takes
- * a class), 1 = generic kernel only, 2 = fast kernels with plain-load staging (no TMA),
- * 3 = row-partitioned fk_blur_fast for RGB as well, 4 = fk_blur_cols for every RGB class,
- * 5 = same as 0.  Adding 16 launches the tap-count classes of a render one after the other on
- * the caller's stream instead of side by side on forked streams.  All variants produce
- * bit-identical output.  Returns the previous value. */
+/* Kernel selection for tests and profiling.  0 = default (RGB frames staged by TMA:
+ * fk_blur_tma; RGB buffers TMA cannot describe: fk_blur_cols; gray: fk_blur_fast; generic
+ * kernel where none of them takes a class), 1 = generic kernel only, 2 = fast kernels with
+ * plain-load staging (no TMA), 3 = row-partitioned fk_blur_fast for RGB as well, 4 =
+ * fk_blur_cols for every RGB class, 5 = same as 0, 6 = fk_blur_tma with one raw buffer.
+ * Adding 16 launches the tap-count classes of a render one after the other on the caller's
+ * stream instead of side by side on forked streams; adding 32 makes the plans built from then
+ * on keep neighbouring fragments with different filters as separate work items instead of
+ * one item with a filter per 8-pixel column.  All variants produce bit-identical output.
+ * Returns the previous value. */
 int fk_set_kernel_variant(fk_handle *h, int variant);
 /* Number of kernel launches issued through this handle so far (bench "gpu_launches"). */
 int64_t fk_launch_count(const fk_handle *h);

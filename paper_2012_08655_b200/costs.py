@@ -55,15 +55,24 @@ def items_macs(items) -> int:
     """Per-channel multiply-accumulates the render kernels execute for one work list
     (DevicePlan.read_items): L * (w * (h + 2r) + w * h) per strip.  Merged strips run the
     horizontal pass over the 2r halo rows between their fragments once, so this is below
-    the algorithmic count of frame_macs, which charges every fragment its own halo."""
+    the algorithmic count of frame_macs, which charges every fragment its own halo.  A mixed
+    item (bit 31 of its last word: a filter per 8-pixel column, radii packed 6 bits each) is
+    the sum over its columns."""
     it = np.asarray(items, dtype=np.int64).reshape(-1, 4)
     if it.size == 0:
         return 0
     w = it[:, 2] & 0xFF
     L = (it[:, 2] >> 8) & 0x1FFF
     h = it[:, 2] >> 21
+    mixed = (it[:, 3] >> 31) & 1
     r = (L - 1) // 2
-    return int(np.where(L > 1, L * (w * (h + 2 * r) + w * h), 0).sum())
+    total = int(np.where((L > 1) & (mixed == 0), L * (w * (h + 2 * r) + w * h), 0).sum())
+    for k in range(4):
+        rk = (it[:, 3] >> (6 * k)) & 63
+        wk = np.clip(w - 8 * k, 0, 8)
+        Lk = 2 * rk + 1
+        total += int(np.where((mixed == 1) & (wk > 0), Lk * (wk * (h + 2 * rk) + wk * h), 0).sum())
+    return total
 
 
 def executed_flops(item_lists, channels: int) -> float:

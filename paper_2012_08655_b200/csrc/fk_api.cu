@@ -379,6 +379,7 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev no_density = {nullptr, 0, 0, 0.0};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
+    p->d.mixed = h->no_mixed ? 0 : 1;
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, no_density, s));
     h->launches++;
     p->n_frames = n_frames;
@@ -444,6 +445,7 @@ int fk_plan_density(fk_plan *p, const fk_params *prm, int n_frames, const double
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev den = {p->density_map, map_w, map_h, sigma_max};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
+    p->d.mixed = h->no_mixed ? 0 : 1;
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, den, s));
     h->launches++;
     p->n_frames = n_frames;
@@ -504,7 +506,8 @@ int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_
     p->custom = 1;
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     p->d.strip_rows = fk_strip_rows_for(1);
-    FK_CUDA(h, fk_launch_order_custom(p->d, s));
+    p->d.mixed = 0; /* a caller's bank: tap offsets are not the canonical r * r */
+    FK_CUDA(h, fk_launch_order(p->d, 1, s));
     h->launches++;
     p->n_frames = 1;
     p->bound_length = lmax;
@@ -615,6 +618,17 @@ static int fk_render_any(fk_handle *h, const fk_plan *p, const void *in, void *o
     if (in == out) return fk_fail(h, FK_EINVAL, "render cannot run in place");
     FK_CUDA(h, cudaSetDevice(h->device));
     int launches = 0;
+    if (p->d.mixed && !(channels == 3 && (h->variant == 0 || h->variant == 5 || h->variant == 6) &&
+                        fk_blur_tma_usable(in, p->d.width, p->d.height, is_f32))) {
+        /* mixed items are read by fk_blur_tma only: this render falls back to another kernel,
+         * so the plan's work lists are emitted once more without them (the cell arrays stay) */
+        fk_plan *pm = const_cast<fk_plan *>(p);
+        pm->d.mixed = 0;
+        FK_CUDA(h, cudaMemsetAsync(pm->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t),
+                                   as_stream(stream)));
+        FK_CUDA(h, fk_launch_order(pm->d, n_frames, as_stream(stream)));
+        launches++;
+    }
     fk_plan_dev pd = p->d;
     if (!p->custom) pd.taps = h->lut32; /* the canonical table may have grown since planning */
     cudaError_t e = fk_launch_blur(h, pd, in, out, n_frames, channels, is_f32,
@@ -642,9 +656,10 @@ int fk_render_f32(fk_handle *h, const fk_plan *p, const float *in_dev, float *ou
 int fk_set_kernel_variant(fk_handle *h, int variant)
 {
     if (!h) return 0;
-    int old = h->variant | (h->serial_classes ? 16 : 0);
+    int old = h->variant | (h->serial_classes ? 16 : 0) | (h->no_mixed ? 32 : 0);
     h->variant = variant & 15;
     h->serial_classes = (variant & 16) != 0;
+    h->no_mixed = (variant & 32) != 0; /* plans made from now on hold no mixed items */
     return old;
 }
 

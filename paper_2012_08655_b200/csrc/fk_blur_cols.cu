@@ -1023,6 +1023,34 @@ __device__ __noinline__ void patch_x_edges_f32(unsigned char *raw, const float *
     for (int j = j0 + (tid & 3); j < n; j += 4) put(j, WC - kC + j % kC);
 }
 
+/*
+ * Filters of an item, per warp (pixel columns [8 w, 8 w + 8) of the strip): a plain item has
+ * one filter; a mixed item (fk_internal.h) one per warp, its radius packed in taps_off and
+ * its taps at r * r of the canonical table.
+ */
+__device__ __forceinline__ int warp_radius(const uint4 q, int warp)
+{
+    return (q.w & FK_ITEM_MIXED) ? (int)((q.w >> (6 * warp)) & 63u)
+                                 : (int)(((q.z >> 8) & 0x1fffu) - 1u) >> 1;
+}
+__device__ __forceinline__ int warp_length(const uint4 q, int warp)
+{
+    return 2 * warp_radius(q, warp) + 1;
+}
+__device__ __forceinline__ uint32_t warp_taps_off(const uint4 q, int warp)
+{
+    const uint32_t r = (uint32_t)warp_radius(q, warp);
+    return (q.w & FK_ITEM_MIXED) ? r * r : q.w;
+}
+/* First 16-byte unit of a row that the TMA box of an item fetches (g.r: the longest filter).
+ * uint8: the chunk that holds the byte three pixels left of the tile -- every warp's stream
+ * starts 3 zpad <= 9 bytes left of ITS tile, which starts at or right of the item's; float32:
+ * the quad of the pixel at or below the tile's first that is a multiple of four (h_float). */
+template <typename T> __device__ __forceinline__ int box_unit(const item_geo &g)
+{
+    return sizeof(T) == 1 ? ((g.x0 - g.r - 3) * kC) >> 4 : (((g.x0 - g.r) & ~3) * kC) >> 2;
+}
+
 /* Three resident CTAs per SM with 167 registers beat four with 127 (27.0 k against 26.8 k
  * frames/s on the bench, 19.4 k against 18.8 k with corner fixations): at 127 the compiler
  * rematerialises addresses and constants inside the task set-up. */
@@ -1062,22 +1090,15 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
      * (possibly left of the image: TMA fills what is outside with zeros) and at the first
      * source row clamped into the image. */
     auto issue = [&](const item_geo &g, int rb, int buf) {
-        /* the H pass's stream starts left of the tile (front-padded taps): uint8 -- 3 zpad
-         * bytes, fetched from the 16-byte chunk that holds the stream's first byte; float32
-         * -- on the pixel at or below the tile's first that is a multiple of four, whose first
-         * float starts a quad (h_float) */
-        const int e0 = kBytes ? (g.x0 - g.r) * C - C * (4 * g.nchunk - g.L)
-                              : ((g.x0 - g.r) & ~3) * C;
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
         mbar_expect_tx(bar + buf, (uint32_t)raw_bytes);
-        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, kBytes ? e0 >> 4 : e0 >> 2,
-                    g.f);
+        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, box_unit<T>(g), g.f);
     };
     auto fill_taps = [&](const uint4 q, int slot) {
-        const int L = (int)((q.z >> 8) & 0x1fffu);
+        const int L = warp_length(q, warp);
         const int n = 4 * ((L + 3) >> 2) + 4;
         const int z = n - 4 - L; /* zeros in front (3 or 1), one zero quad behind */
-        const float *taps = pd.taps + q.w;
+        const float *taps = pd.taps + warp_taps_off(q, warp);
         float *dst = wts + (warp * 3 + slot) * wts_floats;
         for (int i = lane; i < n; i += 32) {
             const int in_range = i >= z && i < z + L;
@@ -1150,40 +1171,45 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
         float *w_h = wts + (warp * 3 + 2) * wts_floats;
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
+        /* Item geometry: g (and r, th, tw: the longest filter of the item) rules what the CTA
+         * shares -- the TMA box, the blocks of tile rows, the clamp-to-edge patch; the warp's
+         * own filter (rw, Lw: the item's, or its column's in a mixed item) rules its taps, the
+         * tile rows its H pass needs -- dw fewer at either end -- and its V pass. */
+        const item_geo g = decode_item<C>(q_cur, W);
+        const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
+        const int th = g.th, tw = g.tw;
+        const int rw = warp_radius(q_cur, warp), Lw = 2 * rw + 1, dw = r - rw;
+        const int nchunk = (Lw + 3) >> 2;
+        const int zpad = 4 * nchunk - Lw;                  /* zeros in front of the taps: 3 or 1 */
+        const int xw = x0 + 8 * warp - rw;                 /* first tile pixel of the warp's columns */
+        const int zf = kBytes ? zpad : xw & 3;             /* zero taps in front, H pass */
+        const int nchunk_h = (zf + Lw + 3) >> 2;
         {
-            const int L = (int)((q_cur.z >> 8) & 0x1fffu);
-            const int zv = 4 * ((L + 3) >> 2) - L; /* zeros in front of w_cur */
             if (kBytes) {
-                const int n = L + zv + 4;
+                const int n = Lw + zpad + 4;
                 for (int i = lane; i < n; i += 32) w_h[i] = w_cur[i] * kTapScaleH;
             } else {
-                const int xr = (int)(q_cur.y & 0xffffu) - ((L - 1) >> 1);
-                const int z = xr & 3;
-                const int n = 4 * ((z + L + 3) >> 2) + 4;
+                const int n = 4 * nchunk_h + 4;
                 for (int i = lane; i < n; i += 32)
-                    w_h[i] = i >= z && i < z + L ? w_cur[i - z + zv] : 0.0f;
+                    w_h[i] = i >= zf && i < zf + Lw ? w_cur[i - zf + zpad] : 0.0f;
             }
             __syncwarp();
         }
-
-        const item_geo g = decode_item<C>(q_cur, W);
-        const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
-        const int nchunk = g.nchunk, th = g.th, tw = g.tw;
-        const int zpad = 4 * nchunk - g.L; /* zeros in front of the taps: 3 or 1 */
         T *dst = out + (size_t)g.f * H * W * C;
-        const int zf = kBytes ? zpad : (x0 - r) & 3;               /* zero taps in front, H pass */
-        const int e0 = (x0 - r - zf) * C;                          /* image element of stream element 0 */
-        const int skew_h = kBytes ? e0 & 15 : 0;                   /* the stream's element 0 in the box */
-        const int nchunk_h = (zf + g.L + 3) >> 2;
-        const int skew = skew_h + C * zpad;                        /* tile float 0 = raw byte skew */
+        const int box0 = box_unit<T>(g) * (kBytes ? 16 : 4); /* image element of the box's first */
+        /* the warp's stream (element 0 meets the first tap, padding included) inside the box */
+        const int sw = (xw - zf) * C - box0;
+        const int skew = (x0 - r) * C - box0;                      /* tile float 0 = raw element skew */
         const int nl = r - x0 > 0 ? r - x0 : 0;                    /* tile pixels left of the image */
         const int nr = x0 + fw + r - W > 0 ? x0 + fw + r - W : 0; /* ... and right of it */
         const int ncol = fw * C - kSegF * warp < kSegF ? fw * C - kSegF * warp : kSegF;
         const bool active = ncol > 0;
+        const int thw = fh + 2 * rw;                               /* tile rows of the warp */
         const int ngroups = (fh + kRV - 1) / kRV;
         const int lead = (2 * r) & (kTB - 1);
         const int n_first = lead == 0 || lead > th ? (th < kTB ? th : kTB) : lead;
-        int vdone = 0, rbm = 0;
+        int vdone = 0;
+        int rbm = dw ? icap - dw : 0; /* ring row of tile row rb: the warp's rows start at tile row dw */
         bool have_next = idx_nxt < n_items;
         for (int rb = 0, nrows = n_first; rb < th; rb += nrows, nrows = th - rb < kTB ? th - rb : kTB) {
             const int ys = y0 - r + rb;
@@ -1203,9 +1229,9 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
                 if (have_next) fill_taps(q_nxt, wslot ^ 1);
             }
             if (!kBytes) {
-                if (e0 < 0 || e0 + tw + C * zf > W * C) {
+                if (box0 < 0 || skew + tw > W * C - box0) {
                     patch_x_edges_f32(raw, reinterpret_cast<const float *>(in) + (size_t)g.f * H * W * C,
-                                      e0, tw + C * zf, W * C, ys_c, H, tid);
+                                      box0, skew + tw, W * C, ys_c, H, tid);
                     __syncthreads();
                 }
             } else if (nl | nr) {
@@ -1250,16 +1276,16 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
                 __syncthreads();
             }
             /* horizontal pass (blockwise.py:151): lane = tile row (clamped in y through the
-             * box row it reads), the warp's 24 columns */
-            if (active && lane < nrows) {
+             * box row it reads), the warp's 24 columns; the rows of the block that lie outside
+             * the warp's own halo (mixed items) are left out */
+            if (active && lane < nrows && rb + lane >= dw && rb + lane < th - dw) {
                 float hacc[kSegF];
                 const int brow = fast_clamp(ys + lane, 0, H - 1) - ys_c; /* box row */
                 if (kBytes)
-                    h_bytes(raw_s + (uint32_t)(brow * kQB), skew_h + kSegF * warp, smem_u32(w_h),
-                            nchunk, zpad, hacc);
+                    h_bytes(raw_s + (uint32_t)(brow * kQB), sw, smem_u32(w_h), nchunk, zpad, hacc);
                 else
-                    h_float(raw_s + (uint32_t)(brow * kQB + (kSegF / 4) * warp * kQStride),
-                            smem_u32(w_h), nchunk_h, zf, 4 * nchunk_h - zf - g.L, hacc);
+                    h_float(raw_s + (uint32_t)(brow * kQB + (sw >> 2) * kQStride), smem_u32(w_h),
+                            nchunk_h, zf, 4 * nchunk_h - zf - Lw, hacc);
                 int rr = rbm + lane + zpad; /* zpad rows down: see v_task_px */
                 rr = rr >= icap ? rr - icap : rr;
                 float *rp = ring + (size_t)(kSegF * warp) * ipitch + rr;
@@ -1287,11 +1313,13 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
             rbm += nrows;
             while (rbm >= icap) rbm -= icap;
 
-            /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) */
-            const int produced = rb + nrows;
+            /* vertical pass (blockwise.py:152) + rounding (convolve.py:15) over the groups of
+             * 8 output rows whose 8 + 2 rw intermediate rows the warp has produced */
+            int produced = rb + nrows - dw;
+            produced = produced > thw ? thw : produced;
             int jend = ngroups;
-            if (produced < th) {
-                const int avail = produced - 2 * r - kRV;
+            if (produced < thw) {
+                const int avail = produced - 2 * rw - kRV;
                 jend = avail >= 0 ? avail / kRV + 1 : 0;
                 jend = jend < ngroups ? jend : ngroups;
             }
@@ -1445,7 +1473,10 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
      * of taps + what the window loads ahead; float32 -- the last warp starts at quad 18 and
      * reads 9 + 3 per chunk of taps */
     const int nq = bytes ? (168 + 6 * r + kQB - 1) / kQB : 18 + 9 + 3 * nchunk_h;
-    const int icap = (2 * r + kTB + 3) & ~3;
+    /* the intermediate: 2r rows the V pass still needs + the 32 of the next block.  A warp of
+     * a mixed item whose filter is shorter than the item's longest is not aligned to the groups
+     * of 8 output rows (up to 7 more rows wait for their group), hence 8 rows of slack */
+    const int icap = (2 * r + kTB + (pd.mixed ? 8 : 0) + 3) & ~3;
     const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
     size_t smem = (size_t)nq * kQStride + 128 +
                   ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
@@ -1489,6 +1520,14 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
 }
 
 } // namespace
+
+bool fk_blur_tma_usable(const void *in, int width, int height, int is_f32)
+{
+    (void)height;
+    if (!get_encode_tiled() || ((uintptr_t)in & 15) != 0) return false;
+    const size_t row = (size_t)width * kC;
+    return is_f32 ? (row & 3) == 0 : (row & 15) == 0;
+}
 
 /* Renders the items of one class list of an RGB batch.  Returns cudaSuccess with
  * *taken = false when the kernel cannot take the class (filters too long for its

@@ -81,8 +81,21 @@ struct fk_item {
     uint32_t frame;
     uint32_t xy;       /* x0 | y0 << 16 */
     uint32_t geom;     /* fw | L << 8 | fh << 21   (fw <= 255, L <= 8191, fh <= 2047) */
-    uint32_t taps_off; /* offset of the L taps inside fk_plan_dev::taps */
+    uint32_t taps_off; /* offset of the L taps inside fk_plan_dev::taps, or FK_ITEM_MIXED | radii */
 };
+/*
+ * Mixed items (fragments narrower than FK_RECT, canonical taps only).  The column-partitioned
+ * kernels give each of their four warps 8 pixels of a strip in BOTH passes, with the warp's own
+ * copy of the taps, so nothing forces the four columns of a strip to share a filter: an
+ * aligned group of FK_RECT / F cells of a grid row whose tap counts differ becomes ONE item
+ * whose taps_off holds FK_ITEM_MIXED and the radius r_w = (L_w - 1) / 2 of the filter of
+ * pixel column 8 w at bits [6 w, 6 w + 6); `L` is the longest of them (it picks the class, the
+ * tile rows and the TMA box), and the taps of radius r start at r * r (the canonical table).
+ * Without them such cells are items 8 or 16 pixels wide that leave three or two warps idle.
+ * Only fk_blur_tma reads mixed items; fk_launch_blur re-emits a plan's items without them
+ * before it has to fall back to another kernel.
+ */
+#define FK_ITEM_MIXED 0x80000000u
 
 /* Device-side view of a plan, passed by value to kernels. */
 struct fk_plan_dev {
@@ -91,6 +104,7 @@ struct fk_plan_dev {
     int nsub_x;          /* strips per fragment across: ceil(fragment / FK_RECT) */
     int nsub_y;          /* strips per fragment down: ceil(fragment / FK_STRIP_ROWS) */
     int strip_rows;      /* tallest strip the plan kernel merges fragments into (fk_strip_rows_for) */
+    int mixed;           /* emit mixed items (FK_ITEM_MIXED) for groups of cells that differ */
     size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */
     fk_item *items;      /* [FK_NCLASS][items_cap] */
     int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors;
@@ -130,6 +144,7 @@ struct fk_handle {
     cudaEvent_t ev_fork = nullptr;
     cudaEvent_t ev_done[kSide] = {};
     int serial_classes = 0; /* fk_set_kernel_variant(v | 16): all classes on the caller's stream */
+    int no_mixed = 0;       /* fk_set_kernel_variant(v | 32): plans without mixed items (A/B runs) */
     /* pipeline resources of fk_foveate_host_* */
     static const int kStreams = 3;
     cudaStream_t streams[kStreams] = {nullptr, nullptr, nullptr};
@@ -177,7 +192,7 @@ int fk_cuda_fail(fk_handle *h, cudaError_t e, const char *what);
 cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cudaStream_t s);
 cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
                            const double *fix_dev, const fk_density_dev &den, cudaStream_t s);
-cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s);
+cudaError_t fk_launch_order(const fk_plan_dev &pd, int n_frames, cudaStream_t s);
 cudaError_t fk_launch_blur(fk_handle *h, const fk_plan_dev &pd, const void *in, void *out,
                            int n_frames, int channels, int is_f32, int bound_length,
                            cudaStream_t s, int *launches);
@@ -187,6 +202,8 @@ cudaError_t fk_launch_blur_fast(fk_handle *h, const fk_plan_dev &pd, int klass, 
 cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, const void *in,
                                 void *out, int n_frames, int is_f32, int class_length,
                                 cudaStream_t s, bool *taken);
+/* true when fk_blur_tma can stage this RGB batch by TMA (16-byte aligned base and rows) */
+bool fk_blur_tma_usable(const void *in, int width, int height, int is_f32);
 cudaError_t fk_launch_fp32_probe(float *buf, int sm_count, int iters, cudaStream_t s);
 /* fk_ssim.cu */
 cudaError_t fk_launch_ssim_map(const uint8_t *ref, const uint8_t *test, int W, int H, int C,

@@ -59,7 +59,8 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  * Fragments up to FK_RECT wide are merged in two steps, both exact (an output pixel depends
  * only on the image and its filter):
  *   across  m = FK_RECT / F neighbouring cells of a grid row (aligned groups after the
- *           leading partial cell) become one unit FK_RECT wide when they share their taps;
+ *           leading partial cell) become one unit FK_RECT wide: one filter when they share
+ *           their taps, else a mixed item with a filter per cell (pd.mixed, fk_internal.h);
  *   down    a vertical run of equal units (same cells, same taps) is cut from its top into
  *           strips of at most pd.strip_rows / F grid rows, which lets the fragments of a
  *           strip share the horizontal pass over the 2r halo rows between them.
@@ -87,41 +88,53 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     if (tid < FK_NCLASS) ccount[tid] = 0;
     __syncthreads();
 
-    /* the unit [u0, u1) of grid row gy that contains cell gx */
-    auto unit_of = [&](int gy, int gx, int &u0, int &u1) {
+    /* The unit [u0, u1) of grid row gy that contains cell gx, and its kind -- 0: the cell
+     * alone; 1: its aligned group of mgrp cells, all with one filter; 2: the group with a filter
+     * per cell (a mixed item, fk_internal.h: every cell blurred, nothing longer than the fast
+     * kernels take, canonical taps). */
+    auto unit_of = [&](int gy, int gx, int &u0, int &u1) -> int {
         u0 = gx;
         u1 = gx + 1;
-        if (mgrp <= 1 || (lead && gx == 0)) return;
+        if (mgrp <= 1 || (lead && gx == 0)) return 0;
         const int g0 = lead + ((gx - lead) / mgrp) * mgrp;
         const int g1 = g0 + mgrp < gw ? g0 + mgrp : gw;
-        if (g1 - g0 < 2) return;
+        if (g1 - g0 < 2) return 0;
         const int32_t *lr = len + gy * gw, *orow = off + gy * gw;
         const int L0 = lr[g0], o0 = orow[g0];
-        if (L0 <= 1) return;
-        for (int x = g0 + 1; x < g1; x++)
-            if (lr[x] != L0 || orow[x] != o0) return;
+        bool same = true;
+        int lmax = 0;
+        for (int x = g0; x < g1; x++) {
+            if (lr[x] <= 1) return 0;
+            same = same && lr[x] == L0 && orow[x] == o0;
+            lmax = lr[x] > lmax ? lr[x] : lmax;
+        }
+        /* a warp's 8 pixel columns must lie in one cell: F = 8 or 16 */
+        if (!same && (!pd.mixed || (F & 7) != 0 || lmax > FK_CLASS_L4)) return 0;
         u0 = g0;
         u1 = g1;
+        return same ? 1 : 2;
     };
     /* Vertical runs of equal units are cut greedily from their top into strips of at most maxc
      * cells.  One thread per grid column walks its column once and records, for every cell,
      * the number of grid rows of the strip it heads (0: headed further up). */
     int32_t *strip = pd.strip + (size_t)f * pd.cap;
     for (int gx = tid; gx < gw; gx += nt) {
-        int head = -1, hu0 = 0, hu1 = 0, hL = 0, ho = 0;
+        int head = -1, hu0 = 0, hu1 = 0, hkind = 0;
         for (int gy = 0; gy < gh; gy++) {
             const int c = gy * gw + gx;
-            int u0 = gx, u1 = gx + 1;
-            const int L = len[c], o = off[c];
-            const bool mergeable = vmerge && L != 1;
-            if (mergeable) unit_of(gy, gx, u0, u1);
+            int u0 = gx, u1 = gx + 1, kind = 0;
+            const bool mergeable = vmerge && len[c] != 1;
+            if (mergeable) kind = unit_of(gy, gx, u0, u1);
             if (gx != u0) { /* inside a unit headed by the cell to its left */
                 strip[c] = 0;
                 head = -1;
                 continue;
             }
-            if (mergeable && head >= 0 && gy - head < maxc && u0 == hu0 && u1 == hu1 && L == hL &&
-                o == ho) {
+            bool joins = mergeable && head >= 0 && gy - head < maxc && u0 == hu0 && u1 == hu1 &&
+                         kind == hkind;
+            for (int x = u0; joins && x < u1; x++) /* the same filter(s) as the head row */
+                joins = len[gy * gw + x] == len[head * gw + x] && off[gy * gw + x] == off[head * gw + x];
+            if (joins) {
                 strip[c] = 0;
                 strip[head * gw + gx] += 1;
             } else {
@@ -129,21 +142,37 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
                 head = mergeable ? gy : -1;
                 hu0 = u0;
                 hu1 = u1;
-                hL = L;
-                ho = o;
+                hkind = kind;
             }
         }
     }
     __syncthreads();
-    /* Cell c heads a strip of n grid rows of the unit [u0, u1); n = 0 when the cell belongs
-     * to a strip headed by another cell. */
-    auto strip_of = [&](int c, int &u0, int &u1) {
+    /* Cell c heads a strip of n grid rows of the unit [u0, u1) of the given kind; n = 0 when the
+     * cell belongs to a strip headed by another cell. */
+    auto strip_of = [&](int c, int &u0, int &u1, int &kind) {
         const int gy = c / gw, gx = c - gy * gw;
         u0 = gx;
         u1 = gx + 1;
+        kind = 0;
         const int n = strip[c];
-        if (n > 0 && merge && len[c] != 1) unit_of(gy, gx, u0, u1);
+        if (n > 0 && merge && len[c] != 1) kind = unit_of(gy, gx, u0, u1);
         return n;
+    };
+    /* longest filter of a unit, and the packed radii of a mixed one: pixel column 8 w of the
+     * unit lies in cell u0 + 8 w / F (every cell of a group but the last is F wide) */
+    auto unit_filters = [&](int c, int u0, int u1, int kind, int &lmax, uint32_t &toff) {
+        lmax = len[c];
+        toff = (uint32_t)off[c];
+        if (kind != 2) return;
+        const int gy = c / gw;
+        toff = FK_ITEM_MIXED;
+        for (int w = 0; w < FK_RECT / 8; w++) {
+            const int x = u0 + (8 * w) / F;
+            if (x >= u1) break;
+            const int L = len[gy * gw + x];
+            lmax = L > lmax ? L : lmax;
+            toff |= (uint32_t)((L - 1) >> 1) << (6 * w);
+        }
     };
     /* rectangle s of the strip headed by cell c; false when it is empty, which happens for
      * clipped fragments wider than FK_RECT */
@@ -167,12 +196,14 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     };
 
     for (int c = tid; c < ncells; c += nt) {
-        int u0, u1;
-        const int n = strip_of(c, u0, u1);
+        int u0, u1, kind, lmax;
+        uint32_t toff;
+        const int n = strip_of(c, u0, u1, kind);
         if (n == 0) continue;
+        unit_filters(c, u0, u1, kind, lmax, toff);
         int cnt = 0, a, b2, w, h2;
         for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, u1, s, a, b2, w, h2) ? 1 : 0;
-        if (cnt) atomicAdd(&ccount[fk_class_of(len[c])], cnt);
+        if (cnt) atomicAdd(&ccount[fk_class_of(lmax)], cnt);
     }
     __syncthreads();
     if (tid == 0) { /* one reservation per class keeps a frame's items contiguous */
@@ -183,10 +214,11 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     }
     __syncthreads();
     for (int c = tid; c < ncells; c += nt) {
-        int u0, u1;
-        const int n = strip_of(c, u0, u1);
+        int u0, u1, kind, L;
+        uint32_t toff;
+        const int n = strip_of(c, u0, u1, kind);
         if (n == 0) continue;
-        const int L = len[c];
+        unit_filters(c, u0, u1, kind, L, toff);
         const int k = fk_class_of(L);
         int cnt = 0, rx0, ry0, fw, fh;
         for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, u1, s, rx0, ry0, fw, fh) ? 1 : 0;
@@ -198,9 +230,38 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
             it.frame = (uint32_t)f;
             it.xy = (uint32_t)rx0 | ((uint32_t)ry0 << 16);
             it.geom = (uint32_t)fw | ((uint32_t)L << 8) | ((uint32_t)fh << 21);
-            it.taps_off = (uint32_t)off[c];
+            it.taps_off = toff;
             *dst++ = it;
         }
+    }
+}
+
+/* Frame f as plain copies (a frame whose fixation lies outside the image). */
+__device__ void fk_emit_copy_through(const fk_plan_dev &pd, int f, bool count_bad)
+{
+    const int W = pd.width, H = pd.height, tid = threadIdx.x;
+    const int ncx = (W + 254) / 255, ncy = (H + 2046) / 2047;
+    if (ncx * ncy <= pd.cap) {
+        __shared__ int s_base;
+        if (tid == 0) {
+            if (count_bad) atomicAdd(&pd.counters[FK_COUNTER_BAD], 1);
+            s_base = atomicAdd(&pd.counters[FK_CLASS_COPY], ncx * ncy);
+        }
+        __syncthreads();
+        fk_item *dst = pd.items + (size_t)FK_CLASS_COPY * pd.items_cap + s_base;
+        for (int i = tid; i < ncx * ncy; i += blockDim.x) {
+            const int cy = i / ncx, cx = i - cy * ncx;
+            const int x0 = cx * 255, y0 = cy * 2047;
+            const int fw = W - x0 < 255 ? W - x0 : 255, fh = H - y0 < 2047 ? H - y0 : 2047;
+            fk_item it;
+            it.frame = (uint32_t)f;
+            it.xy = (uint32_t)x0 | ((uint32_t)y0 << 16);
+            it.geom = (uint32_t)fw | (1u << 8) | ((uint32_t)fh << 21);
+            it.taps_off = 0;
+            dst[i] = it;
+        }
+    } else if (tid == 0 && count_bad) {
+        atomicAdd(&pd.counters[FK_COUNTER_BAD], 1);
     }
 }
 
@@ -221,29 +282,7 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
         /* the host raises ValueError (fk_plan_status); the frame is copied through so that
          * the output buffer is defined whatever the caller does with the error */
         if (tid < FK_META_WORDS) meta[tid] = tid == FK_META_STATUS ? 1 : 0;
-        const int ncx = (W + 254) / 255, ncy = (H + 2046) / 2047;
-        if (ncx * ncy <= pd.cap) {
-            __shared__ int s_base;
-            if (tid == 0) {
-                atomicAdd(&pd.counters[FK_COUNTER_BAD], 1);
-                s_base = atomicAdd(&pd.counters[FK_CLASS_COPY], ncx * ncy);
-            }
-            __syncthreads();
-            fk_item *dst = pd.items + (size_t)FK_CLASS_COPY * pd.items_cap + s_base;
-            for (int i = tid; i < ncx * ncy; i += blockDim.x) {
-                const int cy = i / ncx, cx = i - cy * ncx;
-                const int x0 = cx * 255, y0 = cy * 2047;
-                const int fw = W - x0 < 255 ? W - x0 : 255, fh = H - y0 < 2047 ? H - y0 : 2047;
-                fk_item it;
-                it.frame = (uint32_t)f;
-                it.xy = (uint32_t)x0 | ((uint32_t)y0 << 16);
-                it.geom = (uint32_t)fw | (1u << 8) | ((uint32_t)fh << 21);
-                it.taps_off = 0;
-                dst[i] = it;
-            }
-        } else if (tid == 0) {
-            atomicAdd(&pd.counters[FK_COUNTER_BAD], 1);
-        }
+        fk_emit_copy_through(pd, f, true);
         return;
     }
     const long long ifx = (long long)floor(fx), ify = (long long)floor(fy);
@@ -331,11 +370,18 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
     fk_emit_items(pd, f, ncells);
 }
 
-/* Item emission for a caller-supplied grid (fk_plan_set_grid): frame 0 only. */
-__global__ void __launch_bounds__(FK_PLAN_THREADS) fk_order_kernel(fk_plan_dev pd)
+/* Item emission from the cell arrays of a plan: a caller-supplied grid (fk_plan_set_grid), or
+ * the work lists of a planned batch once more with other settings (pd.mixed). */
+__global__ void __launch_bounds__(FK_PLAN_THREADS) fk_order_kernel(fk_plan_dev pd, int n_frames)
 {
-    const int32_t *meta = pd.meta;
-    fk_emit_items(pd, 0, meta[FK_META_GW] * meta[FK_META_GH]);
+    const int f = blockIdx.x;
+    if (f >= n_frames) return;
+    const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
+    if (meta[FK_META_STATUS] != 0) {
+        fk_emit_copy_through(pd, f, false);
+        return;
+    }
+    fk_emit_items(pd, f, meta[FK_META_GW] * meta[FK_META_GH]);
 }
 
 /* filters.py:30-38 at sigma = L/6 (filters.py:78): one CTA per odd length. */
@@ -390,8 +436,8 @@ cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_fr
     return cudaGetLastError();
 }
 
-cudaError_t fk_launch_order_custom(const fk_plan_dev &pd, cudaStream_t s)
+cudaError_t fk_launch_order(const fk_plan_dev &pd, int n_frames, cudaStream_t s)
 {
-    fk_order_kernel<<<1, FK_PLAN_THREADS, 0, s>>>(pd);
+    fk_order_kernel<<<n_frames, FK_PLAN_THREADS, 0, s>>>(pd, n_frames);
     return cudaGetLastError();
 }
