@@ -192,6 +192,31 @@ int fk_set_kernel_variant(fk_handle *h, int variant);
 /* Number of kernel launches issued through this handle so far (bench "gpu_launches"). */
 int64_t fk_launch_count(const fk_handle *h);
 
+/* ---- request: one gaze-contingent frame as ONE graph launch ------------------------- */
+/* The per-message work of the reference's streaming loop (service.py:192-238: apply the
+ * fixation, render_frame service.py:73-81, send the frame) for an image that stays in HBM:
+ * fixation upload -> plan (retinal model) -> render -> frame and plan summary to pinned host
+ * memory, captured once as a CUDA graph for fixed parameters and buffers and replayed per
+ * request, so a request costs one launch call and no synchronising read-back.
+ *   fk_request_create  captures on `stream` (not the legacy default stream).  `p` must be a
+ *                      one-frame-or-larger plan of the image's geometry and stays bound to the
+ *                      request; in_dev / out_dev are [H][W][C] device buffers, out_host (may be
+ *                      NULL) pinned host memory of the same size.  The graph holds the class
+ *                      launches of the longest filter any fixation inside the image can need.
+ *   fk_request_launch  queues one request for fixation (fx, fy) -- which must lie inside the
+ *                      image, the caller clamps as service.py:58-63 does -- on `stream`.
+ *   fk_request_info    pinned host words, valid once the stream has been synchronised:
+ *                      [0, 8) the frame's plan header (fk_plan_read_lengths), [8] frames whose
+ *                      fixation was rejected on the device (0 or 1), [16, 16 + cells) the tap
+ *                      counts of the fragments, row-major grid_h x grid_w. */
+typedef struct fk_request fk_request;
+int fk_request_create(fk_handle *h, fk_plan *p, const fk_params *params, const void *in_dev,
+                      void *out_dev, void *out_host, int channels, int is_f32, void *stream,
+                      fk_request **out);
+int fk_request_launch(fk_request *r, double fx, double fy, void *stream);
+const int32_t *fk_request_info(const fk_request *r);
+int fk_request_destroy(fk_request *r);
+
 /* ---- foveate: host frames in, host frames out (the call a foveakit user makes) ----- */
 /* Replaces foveate() (blockwise.py:223-243) for a batch held in HOST memory: pipelines
  * H2D copy -> plan -> render -> D2H copy over internal streams in chunks of

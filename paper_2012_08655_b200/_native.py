@@ -23,7 +23,8 @@ EXPORTS = [
     "fk_plan_density", "fk_plan_set_grid", "fk_plan_read", "fk_plan_read_lengths",
     "fk_plan_status", "fk_plan_item_classes", "fk_plan_read_items", "fk_render_u8",
     "fk_render_f32", "fk_set_kernel_variant", "fk_launch_count", "fk_foveate_host_u8",
-    "fk_foveate_host_f32", "fk_host_alloc", "fk_host_free", "fk_measure_fp32_peak", "fk_ssim_u8", "fk_ssim_stats",
+    "fk_foveate_host_f32", "fk_request_create", "fk_request_launch", "fk_request_info",
+    "fk_request_destroy", "fk_host_alloc", "fk_host_free", "fk_measure_fp32_peak", "fk_ssim_u8", "fk_ssim_stats",
 ]
 
 
@@ -88,6 +89,10 @@ def _declare(lib):
         "fk_launch_count": (i64, [vp]),
         "fk_foveate_host_u8": (i32, [vp, P(FkParams), i32, i32, i32, i32, vp, vp, vp, i32]),
         "fk_foveate_host_f32": (i32, [vp, P(FkParams), i32, i32, i32, i32, vp, vp, vp, i32]),
+        "fk_request_create": (i32, [vp, vp, P(FkParams), vp, vp, vp, i32, i32, vp, P(vp)]),
+        "fk_request_launch": (i32, [vp, dbl, dbl, vp]),
+        "fk_request_info": (P(C.c_int32), [vp]),
+        "fk_request_destroy": (i32, [vp]),
         "fk_host_alloc": (i32, [C.c_size_t, P(vp)]),
         "fk_host_free": (i32, [vp]),
         "fk_measure_fp32_peak": (i32, [vp, P(dbl), P(dbl)]),

@@ -376,7 +376,12 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     }
     p->d.taps = h->lut32;
     p->custom = 0;
-    FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
+    /* a request's plan (fk_request_create) zeroes its counters in the plan kernel and reports
+     * to pinned host memory: no memset and no copy nodes in the captured graph */
+    p->d.self_zero = p->request_info != nullptr && n_frames == 1;
+    p->d.info_out = n_frames == 1 ? p->request_info : nullptr;
+    if (!p->d.self_zero)
+        FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev no_density = {nullptr, 0, 0, 0.0};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
     p->d.mixed = h->no_mixed ? 0 : 1;
@@ -446,6 +451,8 @@ int fk_plan_density(fk_plan *p, const fk_params *prm, int n_frames, const double
     const fk_density_dev den = {p->density_map, map_w, map_h, sigma_max};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
     p->d.mixed = h->no_mixed ? 0 : 1;
+    p->d.self_zero = 0;
+    p->d.info_out = nullptr;
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, den, s));
     h->launches++;
     p->n_frames = n_frames;
@@ -507,6 +514,8 @@ int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     p->d.strip_rows = fk_strip_rows_for(1);
     p->d.mixed = 0; /* a caller's bank: tap offsets are not the canonical r * r */
+    p->d.self_zero = 0;
+    p->d.info_out = nullptr;
     FK_CUDA(h, fk_launch_order(p->d, 1, s));
     h->launches++;
     p->n_frames = 1;
@@ -664,6 +673,119 @@ int fk_set_kernel_variant(fk_handle *h, int variant)
 }
 
 int64_t fk_launch_count(const fk_handle *h) { return h ? h->launches : 0; }
+
+/* ------------------------------------------------------------------- request graph */
+struct fk_request {
+    fk_handle *h = nullptr;
+    fk_plan *p = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    double *fix_host = nullptr;   /* pinned, 2 doubles */
+    int32_t *info_host = nullptr; /* pinned, 16 + cell capacity words */
+};
+
+int fk_request_destroy(fk_request *r)
+{
+    if (!r) return FK_OK;
+    if (r->h) cudaSetDevice(r->h->device);
+    if (r->exec) cudaGraphExecDestroy(r->exec);
+    if (r->graph) cudaGraphDestroy(r->graph);
+    cudaFreeHost(r->fix_host);
+    cudaFreeHost(r->info_host);
+    delete r;
+    return FK_OK;
+}
+
+int fk_request_create(fk_handle *h, fk_plan *p, const fk_params *prm, const void *in_dev,
+                      void *out_dev, void *out_host, int channels, int is_f32, void *stream,
+                      fk_request **out)
+{
+    if (!h || !p || !prm || !in_dev || !out_dev || !out)
+        return fk_fail(h, FK_EINVAL, "NULL argument");
+    if (p->h != h) return fk_fail(h, FK_EINVAL, "plan belongs to another handle");
+    cudaStream_t s = as_stream(stream);
+    if (s == nullptr || s == cudaStreamLegacy)
+        return fk_fail(h, FK_EINVAL, "a request is captured on a stream of its own, not the default stream");
+    FK_CUDA(h, cudaSetDevice(h->device));
+    const int W = p->d.width, H = p->d.height;
+    const size_t frame_bytes = (size_t)W * H * channels * (is_f32 ? 4 : 1);
+    fk_request *r = new fk_request();
+    r->h = h;
+    r->p = p;
+    cudaError_t e = cudaHostAlloc(&r->fix_host, 2 * sizeof(double), cudaHostAllocDefault);
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(&r->info_host, (16 + (size_t)p->d.cap) * sizeof(int32_t), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        fk_request_destroy(r);
+        return fk_cuda_fail(h, e, "cudaHostAlloc(request)");
+    }
+    r->fix_host[0] = W / 2.0;
+    r->fix_host[1] = H / 2.0;
+    memset(r->info_host, 0, (16 + (size_t)p->d.cap) * sizeof(int32_t));
+    /* one plain run first: it validates the arguments, grows the tap table to the longest filter
+     * a fixation on the device can need and sets every kernel attribute -- nothing of which may
+     * happen inside a capture */
+    int rc = fk_plan_model(p, prm, 1, r->fix_host, 0, stream);
+    if (rc == FK_OK) rc = fk_plan_model(p, prm, 1, p->fix_dev, 1, stream);
+    if (rc == FK_OK) rc = fk_render_any(h, p, in_dev, out_dev, 1, channels, is_f32, stream);
+    if (rc == FK_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = fk_fail(h, FK_ECUDA, "request warm-up failed");
+    if (rc != FK_OK) {
+        fk_request_destroy(r);
+        return rc;
+    }
+    e = cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) {
+        fk_request_destroy(r);
+        return fk_cuda_fail(h, e, "cudaStreamBeginCapture");
+    }
+    /* FK_REQUEST_PARTS (tuning runs): bit 0 plan, 1 render, 2 frame copy, 3 plan summary */
+    const char *pe = getenv("FK_REQUEST_PARTS");
+    const int parts = pe ? atoi(pe) : 15;
+    if (parts & 1) {
+        /* pinned host memory is mapped into the device's address space (unified addressing):
+         * the plan kernel reads the fixation from it and writes the plan summary to it */
+        p->request_info = (parts & 8) ? r->info_host : nullptr;
+        rc = fk_plan_model(p, prm, 1, r->fix_host, 1, stream);
+        p->request_info = nullptr;
+    }
+    if (e == cudaSuccess && rc == FK_OK && (parts & 2))
+        rc = fk_render_any(h, p, in_dev, out_dev, 1, channels, is_f32, stream);
+    if (e == cudaSuccess && rc == FK_OK && out_host && (parts & 4))
+        e = cudaMemcpyAsync(out_host, out_dev, frame_bytes, cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaStreamEndCapture(s, &r->graph); /* always: leaves the stream usable */
+    if (rc == FK_OK && e != cudaSuccess) rc = fk_cuda_fail(h, e, "request capture");
+    if (rc == FK_OK && e2 != cudaSuccess) rc = fk_cuda_fail(h, e2, "cudaStreamEndCapture");
+    if (rc == FK_OK) {
+        e = cudaGraphInstantiate(&r->exec, r->graph, 0);
+        if (e != cudaSuccess) rc = fk_cuda_fail(h, e, "cudaGraphInstantiate");
+    }
+    if (rc != FK_OK) {
+        fk_request_destroy(r);
+        return rc;
+    }
+    *out = r;
+    return FK_OK;
+}
+
+int fk_request_launch(fk_request *r, double fx, double fy, void *stream)
+{
+    if (!r) return FK_EINVAL;
+    fk_handle *h = r->h;
+    if (!(fx >= 0 && fx < r->p->d.width && fy >= 0 && fy < r->p->d.height))
+        return fk_fail(h, FK_EINVAL, "fixation (%g, %g) outside %dx%d image", fx, fy,
+                       r->p->d.width, r->p->d.height);
+    FK_CUDA(h, cudaSetDevice(h->device));
+    /* the previous request on this stream has been consumed by its upload node once the
+     * caller synchronised; requests in flight on one stream must not overlap (the graph has
+     * one set of buffers) */
+    r->fix_host[0] = fx;
+    r->fix_host[1] = fy;
+    FK_CUDA(h, cudaGraphLaunch(r->exec, as_stream(stream)));
+    h->launches += 1;
+    return FK_OK;
+}
+
+const int32_t *fk_request_info(const fk_request *r) { return r ? r->info_host : nullptr; }
 
 /* ------------------------------------------------------------ host-buffer pipeline */
 static int fk_foveate_host_any(fk_handle *h, const fk_params *prm, int W, int H, int C, int N,

@@ -23,6 +23,7 @@ enum {
 
 #define FK_LUT_DEFAULT_MAX 255
 #define FK_PLAN_THREADS 256
+#define FK_PLAN_THREADS_MAX 1024
 
 /*
  * Work items.  The plan kernel turns the fragments of a frame into strips: rectangles at
@@ -105,6 +106,9 @@ struct fk_plan_dev {
     int nsub_y;          /* strips per fragment down: ceil(fragment / FK_STRIP_ROWS) */
     int strip_rows;      /* tallest strip the plan kernel merges fragments into (fk_strip_rows_for) */
     int mixed;           /* emit mixed items (FK_ITEM_MIXED) for groups of cells that differ */
+    int self_zero;       /* one-frame plans: the plan kernel zeroes `counters` itself (no memset node) */
+    int32_t *info_out;   /* optional host-mapped words the plan kernel fills for frame 0:
+                            [0, 8) meta, [8] rejected fixations, [16, 16 + cells) tap counts */
     size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */
     fk_item *items;      /* [FK_NCLASS][items_cap] */
     int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors;
@@ -170,6 +174,7 @@ struct fk_plan {
     double *fix_dev = nullptr; /* [max_frames][2] staging for host fixations */
     uint8_t *density_map = nullptr; /* device copy of the last density map */
     size_t density_cap = 0;
+    int32_t *request_info = nullptr; /* set around the capture of a request: fk_plan_dev::info_out */
     fk_plan_dev d{};
 };
 

@@ -68,13 +68,14 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  * way (a 64-pixel fragment is two columns, each the head of its own strips), and only
  * fragments taller than FK_STRIP_ROWS are cut into pieces without merging.
  */
-__device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
+__device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const int32_t *len,
+                              const int32_t *off, int32_t *strip)
 {
+    /* len / off / strip: the frame's cell arrays -- the CTA's shared-memory copies when they
+     * fit (the walks below are chains of dependent loads), else the plan's global arrays */
     __shared__ int ccount[FK_NCLASS];
     __shared__ int cbase[FK_NCLASS];
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int32_t *len = pd.length + (size_t)f * pd.cap;
-    const int32_t *off = pd.offset + (size_t)f * pd.cap;
     const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
     const int sx = meta[FK_META_SX], sy = meta[FK_META_SY];
     const int gw = meta[FK_META_GW], gh = meta[FK_META_GH];
@@ -117,7 +118,6 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
     /* Vertical runs of equal units are cut greedily from their top into strips of at most maxc
      * cells.  One thread per grid column walks its column once and records, for every cell,
      * the number of grid rows of the strip it heads (0: headed further up). */
-    int32_t *strip = pd.strip + (size_t)f * pd.cap;
     for (int gx = tid; gx < gw; gx += nt) {
         int head = -1, hu0 = 0, hu1 = 0, hkind = 0;
         for (int gy = 0; gy < gh; gy++) {
@@ -206,11 +206,9 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells)
         if (cnt) atomicAdd(&ccount[fk_class_of(lmax)], cnt);
     }
     __syncthreads();
-    if (tid == 0) { /* one reservation per class keeps a frame's items contiguous */
-        for (int k = 0; k < FK_NCLASS; k++) {
-            cbase[k] = ccount[k] ? atomicAdd(&pd.counters[k], ccount[k]) : 0;
-            ccount[k] = 0; /* becomes the running slot inside the reservation */
-        }
+    if (tid < FK_NCLASS) { /* one reservation per class keeps a frame's items contiguous */
+        cbase[tid] = ccount[tid] ? atomicAdd(&pd.counters[tid], ccount[tid]) : 0;
+        ccount[tid] = 0; /* becomes the running slot inside the reservation */
     }
     __syncthreads();
     for (int c = tid; c < ncells; c += nt) {
@@ -265,10 +263,11 @@ __device__ void fk_emit_copy_through(const fk_plan_dev &pd, int f, bool count_ba
     }
 }
 
-__global__ void __launch_bounds__(FK_PLAN_THREADS)
+__global__ void __launch_bounds__(FK_PLAN_THREADS_MAX)
 fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, int n_frames,
-               fk_density_dev den)
+               fk_density_dev den, int cells_in_smem)
 {
+    extern __shared__ int32_t sm_cells[]; /* [3][cap]: length, offset, strip (cells_in_smem) */
     __shared__ int s_lmax;
     const int f = blockIdx.x;
     if (f >= n_frames) return;
@@ -276,12 +275,17 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
     const int W = pd.width, H = pd.height, F = pd.fragment;
     const double fx = fix[2 * f], fy = fix[2 * f + 1];
     int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
+    if (pd.self_zero) { /* a one-frame plan: this CTA is the only writer of the counters */
+        if (tid < FK_COUNTER_WORDS) pd.counters[tid] = 0;
+        __syncthreads();
+    }
 
     /* retinal.py:73: fixation must satisfy 0 <= fx < w and 0 <= fy < h (NaN fails) */
     if (!(fx >= 0.0 && fx < (double)W && fy >= 0.0 && fy < (double)H)) {
         /* the host raises ValueError (fk_plan_status); the frame is copied through so that
          * the output buffer is defined whatever the caller does with the error */
         if (tid < FK_META_WORDS) meta[tid] = tid == FK_META_STATUS ? 1 : 0;
+        if (pd.info_out && f == 0 && tid < 9) pd.info_out[tid] = tid >= FK_META_STATUS ? 1 : 0;
         fk_emit_copy_through(pd, f, true);
         return;
     }
@@ -305,6 +309,9 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
     int32_t *raw = pd.raw_length + (size_t)f * pd.cap;
     int32_t *len = pd.length + (size_t)f * pd.cap;
     int32_t *off = pd.offset + (size_t)f * pd.cap;
+    int32_t *len_s = cells_in_smem ? sm_cells : len;
+    int32_t *off_s = cells_in_smem ? sm_cells + pd.cap : off;
+    int32_t *strip_s = cells_in_smem ? sm_cells + 2 * pd.cap : pd.strip + (size_t)f * pd.cap;
     int lmax = 1;
     for (int c = tid; c < ncells; c += blockDim.x) {
         const int gy = c / gw, gx = c - gy * gw;
@@ -352,6 +359,10 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
         len[c] = L;
         const int r = (L - 1) >> 1;
         off[c] = r * r;
+        if (cells_in_smem) {
+            len_s[c] = L;
+            off_s[c] = r * r;
+        }
         lmax = L > lmax ? L : lmax;
     }
     atomicMax(&s_lmax, lmax);
@@ -367,13 +378,20 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
         meta[FK_META_STATUS] = 0;
     }
     __syncthreads();
-    fk_emit_items(pd, f, ncells);
+    if (pd.info_out && f == 0) { /* the request's plan summary, straight into pinned host memory */
+        if (tid < FK_META_WORDS) pd.info_out[tid] = meta[tid];
+        if (tid == FK_META_WORDS) pd.info_out[tid] = 0;
+        for (int c = tid; c < ncells; c += blockDim.x) pd.info_out[16 + c] = len_s[c];
+    }
+    fk_emit_items(pd, f, ncells, len_s, off_s, strip_s);
 }
 
 /* Item emission from the cell arrays of a plan: a caller-supplied grid (fk_plan_set_grid), or
  * the work lists of a planned batch once more with other settings (pd.mixed). */
-__global__ void __launch_bounds__(FK_PLAN_THREADS) fk_order_kernel(fk_plan_dev pd, int n_frames)
+__global__ void __launch_bounds__(FK_PLAN_THREADS_MAX)
+fk_order_kernel(fk_plan_dev pd, int n_frames, int cells_in_smem)
 {
+    extern __shared__ int32_t sm_cells[];
     const int f = blockIdx.x;
     if (f >= n_frames) return;
     const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
@@ -381,7 +399,20 @@ __global__ void __launch_bounds__(FK_PLAN_THREADS) fk_order_kernel(fk_plan_dev p
         fk_emit_copy_through(pd, f, false);
         return;
     }
-    fk_emit_items(pd, f, meta[FK_META_GW] * meta[FK_META_GH]);
+    const int ncells = meta[FK_META_GW] * meta[FK_META_GH];
+    const int32_t *len = pd.length + (size_t)f * pd.cap, *off = pd.offset + (size_t)f * pd.cap;
+    int32_t *strip = pd.strip + (size_t)f * pd.cap;
+    if (cells_in_smem) {
+        for (int c = threadIdx.x; c < ncells; c += blockDim.x) {
+            sm_cells[c] = len[c];
+            sm_cells[pd.cap + c] = off[c];
+        }
+        __syncthreads();
+        len = sm_cells;
+        off = sm_cells + pd.cap;
+        strip = sm_cells + 2 * pd.cap;
+    }
+    fk_emit_items(pd, f, ncells, len, off, strip);
 }
 
 /* filters.py:30-38 at sigma = L/6 (filters.py:78): one CTA per odd length. */
@@ -429,15 +460,36 @@ cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cud
     return cudaGetLastError();
 }
 
+/* Dynamic shared memory for a frame's cell arrays (length, offset, strip), 0 when they do not
+ * fit: the kernels then walk the plan's global arrays. */
+static size_t cell_smem_bytes(const fk_plan_dev &pd)
+{
+    const size_t need = 3 * (size_t)pd.cap * sizeof(int32_t);
+    return need <= 160 * 1024 ? need : 0;
+}
+
 cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
                            const double *fix_dev, const fk_density_dev &den, cudaStream_t s)
 {
-    fk_plan_kernel<<<n_frames, FK_PLAN_THREADS, 0, s>>>(pd, prm, fix_dev, n_frames, den);
+    const size_t smem = cell_smem_bytes(pd);
+    if (smem > 40 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fk_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    /* a handful of frames (a streaming request plans one): one large CTA per frame, the cell
+     * loop is a chain of fp64 divisions per cell and nothing else runs beside it */
+    const int threads = n_frames <= 16 ? FK_PLAN_THREADS_MAX : FK_PLAN_THREADS;
+    fk_plan_kernel<<<n_frames, threads, smem, s>>>(pd, prm, fix_dev, n_frames, den, smem != 0);
     return cudaGetLastError();
 }
 
 cudaError_t fk_launch_order(const fk_plan_dev &pd, int n_frames, cudaStream_t s)
 {
-    fk_order_kernel<<<n_frames, FK_PLAN_THREADS, 0, s>>>(pd, n_frames);
+    const size_t smem = cell_smem_bytes(pd);
+    if (smem > 40 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fk_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    fk_order_kernel<<<n_frames, n_frames <= 16 ? FK_PLAN_THREADS_MAX : FK_PLAN_THREADS, smem, s>>>(pd, n_frames, smem != 0);
     return cudaGetLastError();
 }

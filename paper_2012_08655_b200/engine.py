@@ -183,6 +183,70 @@ class DevicePlan:
         return lengths, meta
 
 
+class FrameRequest:
+    """One gaze-contingent frame as one CUDA-graph launch (fk_request_*): fixation upload ->
+    plan -> render -> frame and plan summary in pinned host memory, captured for fixed
+    parameters and buffers.  `launch(x, y)` queues a request on the stream the graph was
+    captured on; after that stream has been synchronised `info()` describes the frame.
+    Requests of one object (and of objects sharing a plan) must not be in flight together."""
+
+    def __init__(self, engine: "Engine", plan: DevicePlan, params, src: torch.Tensor,
+                 out: torch.Tensor, host: np.ndarray | None, stream):
+        if not (src.is_cuda and out.is_cuda and src.is_contiguous() and out.is_contiguous()
+                and src.shape == out.shape and src.dtype == out.dtype):
+            raise ValueError("src and out must be matching contiguous CUDA tensors")
+        if src.dtype not in (torch.uint8, torch.float32):
+            raise ValueError(f"frames must be uint8 or float32, got {src.dtype}")
+        h, w, c = src.shape[-3:]
+        if (w, h) != plan.size or src.numel() != h * w * c:
+            raise ValueError(f"grid does not match image {(w, h)}")
+        if host is not None and (host.nbytes != src.numel() * src.element_size()
+                                 or not host.flags.c_contiguous):
+            raise ValueError("host buffer must be C-contiguous and as large as the frame")
+        self.engine, self.plan, self.stream = engine, plan, stream
+        self._keep = (src, out, host)
+        prm = native_params(params, plan.size, True)
+        ptr = C.c_void_p()
+        with engine._lock:
+            check(engine._lib.fk_request_create(
+                engine._h, plan._p, C.byref(prm), C.c_void_p(src.data_ptr()),
+                C.c_void_p(out.data_ptr()), _np_ptr(host) if host is not None else None,
+                int(c), int(src.dtype == torch.float32), engine._stream(stream), C.byref(ptr)),
+                engine._h)
+        self._r = ptr
+        plan.n_frames = 1
+        plan.fix_on_device = True
+        info = engine._lib.fk_request_info(ptr)
+        self._info = np.ctypeslib.as_array(info, shape=(16 + plan.cap,))
+
+    def launch(self, x: float, y: float) -> None:
+        eng = self.engine
+        with eng._lock:
+            check(eng._lib.fk_request_launch(self._r, float(x), float(y),
+                                             eng._stream(self.stream)), eng._h)
+
+    def info(self) -> dict:
+        """Plan summary of the last request (valid after the stream has been synchronised)."""
+        m = self._info
+        if m[7] != 0 or m[8] != 0:
+            raise ValueError("fixation outside image")
+        gw, gh = int(m[2]), int(m[3])
+        return dict(shift=(int(m[0]), int(m[1])), grid=(gw, gh), foveal=(int(m[4]), int(m[5])),
+                    max_length=int(m[6]),
+                    length=m[16:16 + gw * gh].reshape(gh, gw).astype(np.int64))
+
+    def close(self):
+        if self._r:
+            self.engine._lib.fk_request_destroy(self._r)
+            self._r = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Engine:
     """One GPU.  Thread-safe: C calls on the handle are serialised by a lock."""
 

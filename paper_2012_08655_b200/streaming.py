@@ -9,10 +9,12 @@ time is dominated by the host<->device traffic the paper measures
 
 `FoveationStream` is that loop for the B200 path, without the web plumbing: the source image
 is uploaded ONCE and stays in HBM; a worker thread owns a CUDA stream, a one-frame device
-plan and a ring of pinned host buffers; per request it runs plan -> render on its stream and
-copies the frame back asynchronously, so a request costs two kernel launches and one
-device->host copy and no host->device traffic at all.  Requests that arrive while a frame is
-in flight overwrite each other; only the newest is rendered.
+plan and a ring of pinned host buffers.  A request is ONE CUDA-graph launch
+(`engine.FrameRequest`, fk_request_*): 16 bytes of fixation up, plan -> render on the device,
+the frame and its plan summary down to pinned memory -- no per-kernel launch calls and no
+synchronising read-back after the frame.  Graphs are captured per (parameters other than the
+fixation, output slot) the first time a combination is requested.  Requests that arrive while
+a frame is in flight overwrite each other; only the newest is rendered.
 """
 
 from __future__ import annotations
@@ -25,7 +27,7 @@ from dataclasses import replace
 import numpy as np
 import torch
 
-from .engine import DevicePlan, get_engine, pinned_empty
+from .engine import DevicePlan, FrameRequest, get_engine, pinned_empty
 from .imaging import RasterImage
 from .retinal import FoveationParams
 
@@ -65,6 +67,7 @@ class FoveationStream:
             self._dev = [torch.empty_like(self._src) for _ in range(depth)]
         self._host = [pinned_empty(img.shape, np.uint8) for _ in range(depth)]
         self._plans: dict[int, DevicePlan] = {}
+        self._requests: dict = {}
         self._slot = 0
         self._pending = None            # the mailbox: newest request, or None
         self._cv = threading.Condition()
@@ -101,6 +104,9 @@ class FoveationStream:
             self._closed = True
             self._cv.notify()
         self._worker.join()
+        for r in self._requests.values():
+            r.close()
+        self._requests.clear()
         for p in self._plans.values():
             p.close()
         self._plans.clear()
@@ -133,6 +139,21 @@ class FoveationStream:
             self._plans[fragment_size] = p
         return p
 
+    def _request(self, params: FoveationParams, slot: int) -> FrameRequest:
+        """The captured graph for these parameters and this output slot."""
+        key = (replace(params, fixation=None), slot)
+        r = self._requests.get(key)
+        if r is None:
+            if len(self._requests) >= 8 * len(self._dev):   # parameters keep changing: start over
+                self._stream.synchronize()
+                for old in self._requests.values():
+                    old.close()
+                self._requests.clear()
+            r = FrameRequest(self._eng, self._plan(params.fragment_size), params, self._src[0],
+                             self._dev[slot][0], self._host[slot], self._stream)
+            self._requests[key] = r
+        return r
+
     def _run(self):
         torch.cuda.set_device(self._device)
         while True:
@@ -145,19 +166,14 @@ class FoveationStream:
                 self._pending = None
             try:
                 params, clamped = self._apply(x, y, overrides)
-                t0 = time.perf_counter()
                 slot = self._slot
                 self._slot = (slot + 1) % len(self._dev)
-                plan = self._plan(params.fragment_size)
-                fix = np.asarray([params.fixation], dtype=np.float64)
-                with torch.cuda.stream(self._stream):
-                    plan.model(params, fix, stream=self._stream)
-                    self._eng.render(self._src, plan, out=self._dev[slot], stream=self._stream)
-                    host = torch.from_numpy(self._host[slot])
-                    host.copy_(self._dev[slot][0], non_blocking=True)
+                req = self._request(params, slot)
+                t0 = time.perf_counter()
+                req.launch(*params.fixation)
                 self._stream.synchronize()
                 ms = (time.perf_counter() - t0) * 1000.0
-                info = plan.read(0, stream=self._stream)
+                info = req.info()
                 stats = {
                     "render_ms": round(ms, 3),
                     "regions": int(len(np.unique(info["length"]))),

@@ -66,6 +66,72 @@ def test_stream_frames_equal_foveate_and_latest_wins():
             s.submit(1.0, 1.0, gamma=2)
 
 
+@pytest.mark.gpu
+def test_two_streams_on_one_image_size_run_side_by_side():
+    """Two service-style callers on the same geometry (service.py:231: one connection per
+    worker thread): each stream owns its plan, CUDA stream and request graphs, so their
+    frames interleave freely and every one of them still equals foveate()."""
+    import threading
+
+    rng = np.random.default_rng(8)
+    imgs = [rng.integers(0, 256, (270, 480, 3), dtype=np.uint8) for _ in range(2)]
+    pts = [(float(x), float(y)) for x, y in rng.integers(0, 270, (12, 2))]
+    results = [[], []]
+
+    def client(k):
+        with FoveationStream(imgs[k], fk.FoveationParams(fragment_size=32)) as s:
+            for (x, y) in pts:
+                s.submit(x, y)
+                out, stats = s.get(timeout=60)
+                results[k].append((x, y, out.copy()))
+
+    threads = [threading.Thread(target=client, args=(k,)) for k in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(120)
+    for k in range(2):
+        assert len(results[k]) == len(pts)
+        for (x, y, out) in results[k]:
+            ref, *_ = fk.foveate(fk.RasterImage.from_array(imgs[k]),
+                                 fk.FoveationParams(fragment_size=32, fixation=(x, y)))
+            assert np.array_equal(out, ref.data)
+
+
+@pytest.mark.gpu
+def test_frame_request_graph_equals_foveate_float32_and_reports_plan():
+    """fk_request_*: the captured plan -> render -> copy graph on a float32 frame, replayed
+    for several fixations, equals foveate_batch bit for bit and reports the plan header."""
+    import torch
+    from paper_2012_08655_b200.engine import DevicePlan, FrameRequest, get_engine, pinned_empty
+
+    rng = np.random.default_rng(4)
+    frame = torch.from_numpy(rng.random((200, 320, 3), dtype=np.float32)).cuda()
+    out = torch.empty_like(frame)
+    host = pinned_empty((200, 320, 3), np.float32)
+    eng = get_engine(0)
+    params = fk.FoveationParams(fragment_size=16, strength=1.7)
+    plan = DevicePlan(eng, (320, 200), 16, 1)
+    stream = torch.cuda.Stream()
+    req = FrameRequest(eng, plan, params, frame, out, host, stream)
+    try:
+        for (x, y) in [(160.0, 100.0), (0.0, 0.0), (319.0, 199.0), (33.5, 150.25)]:
+            req.launch(x, y)
+            stream.synchronize()
+            ref = fk.foveate_batch(frame[None], np.asarray([[x, y]]), params)[0]
+            assert torch.equal(out, ref)
+            assert np.array_equal(host, ref.cpu().numpy())
+            info = req.info()
+            exp = fk.compute_fragment_shift((x, y), 16)
+            assert info["shift"] == tuple(exp)
+            assert info["length"].shape == (info["grid"][1], info["grid"][0])
+        with pytest.raises(ValueError):
+            req.launch(320.0, 10.0)
+    finally:
+        req.close()
+        plan.close()
+
+
 def test_harness_config_validation_matches_reference():
     # bench.py:48-56: warm-up >= 3, iterations >= 10, no empty axes
     from paper_2012_08655_b200 import harness
