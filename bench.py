@@ -404,7 +404,27 @@ def config_legs(bench, args, rank, world):
             fk.render(img, grid, bank)
         e["e2e_value"] = 10 / (time.perf_counter() - t0)
         e["e2e_api"] = "paper_2012_08655_b200.render(RasterImage, grid, bank) -- host image in and out"
+        # the streaming request (fk_request_*): the image stays in HBM, one graph launch takes a
+        # fixation and returns the frame and its plan summary in pinned host memory
+        from paper_2012_08655_b200.engine import DevicePlan, FrameRequest, get_engine, pinned_empty
+        host = pinned_empty((H5, W5, 3), np.uint8)
+        rplan = DevicePlan(get_engine(torch.cuda.current_device()), (W5, H5), 32, 1)
+        rstream = torch.cuda.Stream()
+        rout = torch.empty_like(fr[0])
+        req = FrameRequest(rplan.engine, rplan, fk.FoveationParams(), fr[0], rout, host, rstream)
+        lat = []
+        for k in range(60):
+            t0 = time.perf_counter()
+            req.launch(W5 / 2.0 + 3 * (k % 7), H5 / 2.0)
+            rstream.synchronize()
+            lat.append(time.perf_counter() - t0)
+        req.close()
+        rplan.close()
+        e["request_ms_median"] = float(np.median(lat[10:]) * 1e3)
+        e["request_api"] = ("FrameRequest.launch(x, y) + stream sync: fixation up, plan, render, "
+                            "frame + plan summary down to pinned host memory, one CUDA graph")
         legs.append(e)
+        del rout, host
         del fr
         done()
         # the per-GPU share of the headline batch at 8 GPUs, on this one GPU

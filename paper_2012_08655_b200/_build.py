@@ -50,24 +50,34 @@ def is_current() -> bool:
     return LIB.exists() and STAMP.exists() and STAMP.read_text().strip() == source_hash()
 
 
-def build_native(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the CUDA sources into csrc/libfovea.so if missing or stale."""
-    if not force and is_current():
+def build_native(force: bool = False, verbose: bool = False, debug_barriers: bool = False) -> Path:
+    """Compile the CUDA sources into csrc/libfovea.so if missing or stale.  debug_barriers
+    builds the racecheck variant (-DFK_DEBUG_CTA_BARRIERS, see fk_blur_cols.cu); the stamp is
+    not written for it, so the next ordinary build replaces it."""
+    if not force and not debug_barriers and is_current():
         return LIB
+    if not force and not debug_barriers and LIB.exists() and os.environ.get("FK_KEEP_BUILD"):
+        return LIB  # tools/racecheck.sh: run whatever was built last, stale stamp or not
     cmd = [_nvcc(), *NVCC_FLAGS]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    if debug_barriers:
+        cmd += ["-DFK_DEBUG_CTA_BARRIERS"]
     cmd += ["-o", str(LIB), *[str(CSRC / s) for s in SOURCES]]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + proc.stdout + proc.stderr)
     if verbose:
         print(proc.stdout + proc.stderr)
-    STAMP.write_text(source_hash() + "\n")
+    if debug_barriers:
+        STAMP.write_text("debug-barriers build\n")
+    else:
+        STAMP.write_text(source_hash() + "\n")
     return LIB
 
 
 if __name__ == "__main__":
     import sys
 
-    print(build_native(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build_native(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                       debug_barriers="--debug-barriers" in sys.argv))

@@ -52,6 +52,20 @@
  */
 #include "fk_stage.cuh"
 
+/*
+ * fk_blur_tma synchronises with mbarriers only ("bytes landed", "H pass done"), which
+ * compute-sanitizer's racecheck does not model.  -DFK_DEBUG_CTA_BARRIERS (python -m
+ * paper_2012_08655_b200._build --debug-barriers, tools/racecheck.sh) adds a CTA barrier next
+ * to each of them -- the mbarriers stay -- so that racecheck can verify everything they order
+ * between threads: the item slots thread 0 publishes, the taps, the intermediate.  (What TMA
+ * writes is invisible to racecheck either way.)
+ */
+#ifdef FK_DEBUG_CTA_BARRIERS
+#define FK_DEBUG_CTA_SYNC() __syncthreads()
+#else
+#define FK_DEBUG_CTA_SYNC()
+#endif
+
 namespace {
 
 constexpr int kC = 3;
@@ -1220,6 +1234,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
             const uint32_t raw_s = smem_u32(raw);
             bc++;
             mbar_wait(bar + buf, phase); /* the block's bytes have landed */
+            FK_DEBUG_CTA_SYNC();
             if (rb == 0) {
                 if (item_no > 0) { /* the next item, published by thread 0 during the previous one */
                     idx_nxt = slot_idx[par ^ 1];
@@ -1293,6 +1308,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
                 for (int j = 0; j < kSegF; j++) rp[j * ipitch] = hacc[j];
             }
             __syncwarp();
+            FK_DEBUG_CTA_SYNC();
             if (lane == 0) mbar_arrive(hbar + buf); /* this warp is through with the raw bytes */
             if (warp == 0) {
                 /* every warp is through with this buffer: publish the drawn item, then request

@@ -525,3 +525,127 @@ def test_strip_height_does_not_change_the_output():
         assert res.returncode == 0, res.stderr[-2000:]
         digests[force] = res.stdout.strip().splitlines()[-1]
     assert len(set(digests.values())) == 1, digests
+
+
+# ------------------------------------------------- BASELINE configs at their named shapes
+@pytest.mark.parametrize("F,e2", [(32, 2.3), (16, 1.5), (8, 2.3), (64, 1.5)])
+def test_f32_1080p_named_shape_vs_oracle(F, e2):
+    """BASELINE config 5 at its named shape: a 1920x1080 float32 frame, centre fixation, default
+    and steeper fit, every block size, against the C oracle (unquantised), and -- the same
+    arithmetic -- bit for bit against the generic kernel.  F = 8 and 16 run as mixed items."""
+    img = frame_f32(70 + F, (1080, 1920, 3))
+    kw = dict(fragment_size=F, e2=e2)
+    p = fk.FoveationParams(**kw)
+    dev = torch.from_numpy(img)[None].cuda()
+    out = fk.foveate_batch(dev, None, p)
+    ref, _ = fo.c_foveate(img, fo.OracleParams(**kw), quantize=False, threads=8)
+    err = np.abs(out[0].cpu().numpy().astype(np.float64) - ref)
+    assert np.all(err <= F32_RTOL * np.maximum(np.abs(ref), 1.0)), float(err.max())
+    eng = fk.get_engine(0)
+    eng.set_kernel_variant(1)
+    try:
+        gen = fk.foveate_batch(dev, None, p)
+    finally:
+        eng.set_kernel_variant(0)
+    assert torch.equal(out, gen)
+
+
+def test_gray_1080p_vs_oracle():
+    """Single-channel frames at full size (the row-partitioned fk_blur_fast path)."""
+    img = frame_u8(81, (1080, 1920, 1))
+    for fix in ((960.0, 540.0), (1919.0, 0.0)):
+        out = fk.foveate_batch(torch.from_numpy(img)[None].cuda(), np.asarray([fix]),
+                               fk.FoveationParams())[0].cpu().numpy()
+        ref, _ = fo.c_foveate(img, fo.OracleParams(fixation=fix), threads=8)
+        assert maxdiff(out, ref) <= U8_TOL
+        assert (out != ref).mean() < 2e-3
+
+
+@pytest.mark.parametrize("W", [1921, 1918])
+def test_row_pitch_not_a_multiple_of_16_bytes_vs_oracle(W):
+    """W * C % 16 != 0: TMA cannot describe the rows, the render leaves fk_blur_tma for
+    fk_blur_cols with plain-load staging (and, for 16-pixel fragments, emits the plan's items
+    again without mixed ones); the result still matches the oracle."""
+    img = frame_u8(82 + W, (270, W, 3))
+    for F in (32, 16):
+        kw = dict(fragment_size=F, fixation=(W - 5.0, 100.0))
+        out, *_ = fk.foveate(fk.RasterImage.from_array(img), fk.FoveationParams(**kw))
+        ref, _ = fo.c_foveate(img, fo.OracleParams(**kw), threads=8)
+        assert maxdiff(out.data, ref) <= U8_TOL
+    f32 = frame_f32(83, (120, W, 3))
+    p = fk.FoveationParams(fragment_size=16, fixation=(3.0, 3.0))
+    out = fk.foveate_batch(torch.from_numpy(f32)[None].cuda(), np.asarray([[3.0, 3.0]]), p)[0].cpu().numpy()
+    ref, _ = fo.c_foveate(f32, fo.OracleParams(fragment_size=16, fixation=(3.0, 3.0)), quantize=False, threads=8)
+    assert np.all(np.abs(out.astype(np.float64) - ref) <= F32_RTOL * np.maximum(np.abs(ref), 1.0))
+
+
+def test_rl_batch_65536_frames_named_shape_vs_oracle():
+    """BASELINE config 4 at its named size: 65 536 frames of 256x256 RGB (12.9 GB in, 12.9 GB
+    out), random fixations.  64 frames spread over the whole batch -- the last one included, so
+    the item / frame offsets at the top of the range are exercised -- against the C oracle, and
+    a checksum property over all of them: a frame whose fixation and content are duplicated
+    elsewhere in the batch comes out identical."""
+    n = 65536
+    free, _total = torch.cuda.mem_get_info()
+    if free < 30 * 2**30:
+        pytest.skip("needs 30 GB of free device memory")
+    g = torch.Generator(device="cuda").manual_seed(4)
+    frames = torch.randint(0, 256, (n, 256, 256, 3), dtype=torch.uint8, device="cuda", generator=g)
+    rng = np.random.default_rng(1)
+    fix = np.stack([rng.integers(0, 256, n), rng.integers(0, 256, n)], axis=1).astype(np.float64)
+    # duplicates: frame n-1-k repeats frame k for the first 16 frames
+    frames[n - 16:] = frames[:16].flip(0)
+    fix[n - 16:] = fix[:16][::-1]
+    out = fk.foveate_batch(frames, fix, fk.FoveationParams())
+    assert torch.equal(out[n - 16:], out[:16].flip(0))
+    picks = sorted(set(np.linspace(0, n - 1, 64).astype(int).tolist()))
+    for i in picks:
+        ref, _ = fo.c_foveate(frames[i].cpu().numpy(), fo.OracleParams(fixation=tuple(fix[i])), threads=8)
+        assert maxdiff(out[i].cpu().numpy(), ref) <= U8_TOL, i
+    del frames, out
+    torch.cuda.empty_cache()
+
+
+def test_mixed_items_every_width_and_filter_combination_vs_generic_and_oracle():
+    """Fragments of 8 and 16 pixels: neighbouring cells with different filters render as one
+    strip with a filter per warp (fk_internal.h, FK_ITEM_MIXED).  Bit-identical to the generic
+    kernel and to the same plans without mixed items, on uint8 and float32, including fixations
+    at the corners (longest filters, clamped halos) and widths that clip the last group; one
+    frame of each also against the oracle."""
+    rng = np.random.default_rng(21)
+    eng = fk.get_engine(0)
+    for (h, w, F) in [(96, 176, 8), (200, 336, 16), (64, 80, 8), (130, 496, 16)]:
+        n = 5
+        fix = np.stack([rng.uniform(0, w, n), rng.uniform(0, h, n)], axis=1)
+        fix[0], fix[1], fix[2] = (0.0, 0.0), (w - 1.0, h - 1.0), (w - 1.0, 0.0)
+        p = fk.FoveationParams(fragment_size=F, strength=2.2, e2=1.4)
+        for dtype in (np.uint8, np.float32):
+            host = (rng.integers(0, 256, (n, h, w, 3), dtype=np.uint8) if dtype == np.uint8
+                    else rng.random((n, h, w, 3), dtype=np.float32))
+            frames = torch.from_numpy(host).cuda()
+            got = fk.foveate_batch(frames, fix, p).clone()
+            try:
+                eng.set_kernel_variant(1)
+                gen = fk.foveate_batch(frames, fix, p).clone()
+                eng.set_kernel_variant(32)
+                plain = fk.foveate_batch(frames, fix, p).clone()
+            finally:
+                eng.set_kernel_variant(0)
+            assert torch.equal(got, gen) and torch.equal(got, plain)
+            ref, _ = fo.c_foveate(host[3], fo.OracleParams(fragment_size=F, strength=2.2, e2=1.4,
+                                                           fixation=tuple(fix[3])),
+                                  quantize=dtype == np.uint8, threads=8)
+            if dtype == np.uint8:
+                assert maxdiff(got[3].cpu().numpy(), ref) <= U8_TOL
+            else:
+                err = np.abs(got[3].cpu().numpy().astype(np.float64) - ref)
+                assert np.all(err <= F32_RTOL * np.maximum(np.abs(ref), 1.0))
+    # the plan really holds mixed items, and the accounting reads them
+    from paper_2012_08655_b200 import costs
+    plan = eng.plan_for((336, 200), 16, 1)
+    plan.model(fk.FoveationParams(fragment_size=16, strength=2.2), np.asarray([[100.0, 60.0]]))
+    items = np.concatenate(plan.read_items()[:-1])
+    assert (items[:, 3] >> 31).any()
+    lengths, meta = plan.read_lengths()
+    alg = costs.batch_flops((336, 200), 16, 3, lengths, meta)
+    assert 0 < costs.executed_flops(plan.read_items()[:-1], 3) <= alg
