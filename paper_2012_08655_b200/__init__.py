@@ -3,14 +3,14 @@
 kernels behind a C ABI (include/fovea.h, csrc/).
 
 Only the hot path and its "next" rows are here: plan / render /
-foveate, density-map sigma fields, the latest-wins streaming layer, the timing harness, the
-command line for those (``python -m paper_2012_08655_b200``) and the SSIM checker
-(``quality``).  The reference's web service, pyramid baseline and per-pixel oracle are out of
-scope.  There is no CPU fallback: importing works anywhere, but every compute entry point
+foveate, density-map sigma fields, the latest-wins streaming layer, the SSIM checker
+(``quality``) and ``adapter``, which routes the reference's own command line, timing harness
+and service onto this path when foveakit is importable.  The reference's file codecs, web
+service, pyramid baseline and per-pixel oracle are out of scope.  There is no CPU fallback: importing works anywhere, but every compute entry point
 needs a CUDA device.
 """
 
-from .imaging import RasterImage, load_image, save_image
+from .imaging import RasterImage
 from .retinal import (
     FoveationParams,
     SigmaField,
@@ -48,7 +48,7 @@ from .quality import SSIMMap, mean_ssim_map, ssim_map
 __version__ = "0.1.0"
 
 __all__ = [
-    "RasterImage", "load_image", "save_image", "SSIMMap", "ssim_map", "mean_ssim_map",
+    "RasterImage", "SSIMMap", "ssim_map", "mean_ssim_map",
     "FoveationParams", "SigmaField", "build_sigma_field", "contrast_threshold",
     "cutoff_cpd", "cutoff_cpp", "eccentricity_of", "ingest_density_map", "sigma_at",
     "FilterBank", "build_bank", "filter_length", "gaussian_filter_1d", "total_coefficients",

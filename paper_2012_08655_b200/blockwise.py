@@ -210,6 +210,54 @@ def _check_fixations(fix, n, size):
     return fix
 
 
+def _foveate_shards(shards, fixations, params, out, use_shift, validate):
+    """foveate_batch for a batch that lives on several GPUs as one CUDA tensor per device."""
+    shards = list(shards)
+    for t in shards:
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.ndim == 4):
+            raise ValueError("a sharded batch is a list of CUDA tensors [n_i, H, W, C]")
+    counts = [int(t.shape[0]) for t in shards]
+    if fixations is None:
+        fixations = [None] * len(shards)
+    elif not isinstance(fixations, (list, tuple)):
+        fix = np.asarray(fixations, dtype=np.float64).reshape(-1, 2)
+        if fix.shape[0] != sum(counts):
+            raise ValueError(f"{sum(counts)} frames but {fix.shape[0]} fixations")
+        cuts = np.cumsum([0] + counts)
+        fixations = [fix[cuts[i]:cuts[i + 1]] for i in range(len(shards))]
+    if len(fixations) != len(shards):
+        raise ValueError(f"{len(shards)} shards but {len(fixations)} fixation arrays")
+    outs = list(out) if out is not None else [None] * len(shards)
+    if len(outs) != len(shards):
+        raise ValueError(f"{len(shards)} shards but {len(outs)} output tensors")
+    results, errors = [None] * len(shards), []
+
+    def work(i):
+        t = shards[i]
+        try:
+            if t.shape[0] == 0:
+                results[i] = outs[i] if outs[i] is not None else torch.empty_like(t)
+                return
+            with torch.cuda.device(t.device):
+                stream = torch.cuda.Stream(device=t.device)
+                stream.wait_stream(torch.cuda.current_stream(t.device))
+                with torch.cuda.stream(stream):
+                    results[i] = foveate_batch(t, fixations[i], params, out=outs[i],
+                                               use_shift=use_shift, validate=validate)
+                stream.synchronize()
+        except Exception as exc:  # surfaced after join
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(shards))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    return results
+
+
 def foveate_batch(frames, fixations=None, params: FoveationParams | None = None, *, out=None,
                   devices=None, use_shift: bool = True, chunk_frames: int = 0,
                   validate: bool = True):
@@ -217,7 +265,13 @@ def foveate_batch(frames, fixations=None, params: FoveationParams | None = None,
 
     frames     [N, H, W, C] uint8 or float32, C in {1, 3}: a numpy array (host memory,
                rendered through the pipelined host path and returned as numpy) or a CUDA
-               torch tensor (rendered in place on its GPU and returned as a tensor).
+               torch tensor (rendered in place on its GPU and returned as a tensor) -- or a
+               list of CUDA tensors, the shards of one batch resident on several GPUs
+               (contiguous split, no collective): every shard is planned and
+               rendered on its own GPU by its own host thread and CUDA stream, nothing
+               crosses the host, and the list of output tensors is returned.  `fixations` is
+               then a list with one entry per shard, or one [N_total, 2] array cut in shard
+               order; `out` a list of tensors or None.
     fixations  [N, 2] (x, y) pixel coordinates; default: the image centre
                (``params.fixation`` if set).  For device frames this may be a CUDA
                float64 tensor.
@@ -228,6 +282,8 @@ def foveate_batch(frames, fixations=None, params: FoveationParams | None = None,
                asynchronous and copies such frames through.
     """
     params = params if params is not None else FoveationParams()
+    if isinstance(frames, (list, tuple)):
+        return _foveate_shards(frames, fixations, params, out, use_shift, validate)
     if isinstance(frames, torch.Tensor) and frames.is_cuda:
         n, h, w, _ = frames.shape
         if fixations is None:

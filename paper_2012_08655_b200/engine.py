@@ -248,7 +248,9 @@ class FrameRequest:
 
 
 class Engine:
-    """One GPU.  Thread-safe: C calls on the handle are serialised by a lock."""
+    """One GPU.  Thread-safe: the (short, asynchronous) C calls on the handle are serialised by
+    a lock; the GPU work they queue runs on the caller's stream, and callers on different
+    streams get plans of their own (plan_for), so their kernels overlap."""
 
     def __init__(self, device: int = 0):
         self._lib = _native.lib()
@@ -289,9 +291,13 @@ class Engine:
         return C.c_void_p(int(stream))
 
     # ---------------------------------------------------------------------- plans
-    def plan_for(self, size, fragment_size, n_frames) -> DevicePlan:
-        """A cached DevicePlan able to hold n_frames frames of this geometry."""
-        key = (int(size[0]), int(size[1]), int(fragment_size))
+    def plan_for(self, size, fragment_size, n_frames, stream=None) -> DevicePlan:
+        """A cached DevicePlan able to hold n_frames frames of this geometry, for work queued
+        on `stream` (default: the current stream).  Plans are cached per (geometry, stream): a
+        plan's buffers are rewritten by every call, so callers on different streams -- two
+        service connections on one image size, the shards of a batch -- must not share one."""
+        sid = int(self._stream(stream).value or 0)
+        key = (int(size[0]), int(size[1]), int(fragment_size), sid)
         with self._lock:
             p = self._plans.get(key)
             if p is None or p.max_frames < n_frames:
@@ -354,7 +360,7 @@ class Engine:
         if nfix != n:
             raise ValueError(f"{n} frames but {nfix} fixations")
         with self._lock:
-            plan = self.plan_for((w, h), params.fragment_size, n)
+            plan = self.plan_for((w, h), params.fragment_size, n, stream=stream)
             plan.model(params, fixations, use_shift=use_shift, stream=stream)
             out = self.render(frames, plan, out=out, stream=stream)
             if validate and plan.fix_on_device:

@@ -649,3 +649,23 @@ def test_mixed_items_every_width_and_filter_combination_vs_generic_and_oracle():
     lengths, meta = plan.read_lengths()
     alg = costs.batch_flops((336, 200), 16, 3, lengths, meta)
     assert 0 < costs.executed_flops(plan.read_items()[:-1], 3) <= alg
+
+
+def test_device_resident_shards_one_thread_and_stream_each():
+    """a batch resident on several GPUs as one tensor per device, rendered
+    with no host round trip -- here both shards live on cuda:0, which exercises the per-shard
+    threads, streams and plans; the result equals the unsharded batch."""
+    n = 11
+    frames = torch.from_numpy(frame_u8(90, (n, 180, 320, 3))).cuda()
+    fix = np.random.default_rng(90).uniform(0, 1, (n, 2)) * [320, 180]
+    p = fk.FoveationParams(fragment_size=16)
+    whole = fk.foveate_batch(frames, fix, p)
+    a, b = fk.shard_range(n, 0, 2)
+    shards = [frames[a:b].contiguous(), frames[b:].contiguous()]
+    outs = fk.foveate_batch(shards, fix, p)
+    assert isinstance(outs, list) and len(outs) == 2
+    assert torch.equal(torch.cat(outs), whole)
+    outs2 = fk.foveate_batch(shards, [fix[a:b], fix[b:]], p, out=[torch.empty_like(t) for t in shards])
+    assert torch.equal(torch.cat(outs2), whole)
+    with pytest.raises(ValueError):
+        fk.foveate_batch(shards, fix[:-1], p)

@@ -55,6 +55,54 @@ def test_two_ranks_partition_the_batch_exactly_once():
     assert got["elapsed"] == 2.0               # max over ranks, as bench.py reports
 
 
+def _slice_flops(fix, size, F):
+    """Algorithmic FLOPs of the frames with these fixations: oracle plans (the checker) fed to
+    the product's accounting (costs.batch_flops), as bench.py does with device plans."""
+    from oracle import fovea_oracle as fo
+    from paper_2012_08655_b200 import costs
+
+    cap = (size[0] // F + 2) * (size[1] // F + 2)
+    lengths = np.ones((len(fix), cap), np.int32)
+    meta = np.zeros((len(fix), 8), np.int32)
+    for i, (x, y) in enumerate(fix):
+        pl = fo.np_plan(size, fo.OracleParams(fragment_size=F, fixation=(float(x), float(y))))
+        gh, gw = pl["length"].shape
+        lengths[i, :gw * gh] = pl["length"].reshape(-1)
+        meta[i, :4] = (pl["shift"][0], pl["shift"][1], gw, gh)
+    return costs.batch_flops(size, F, 3, lengths, meta) if len(fix) else 0.0
+
+
+def _cost_worker(rank, world, port, n_frames, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # the strong-scaling split of bench.py: one fixed batch, rank r owns shard_range(n, r, g)
+        rng = np.random.default_rng(1)
+        fix = np.stack([rng.integers(0, 256, n_frames), rng.integers(0, 256, n_frames)], axis=1)
+        a, b = fk.shard_range(n_frames, rank, world)
+        mine = torch.tensor([_slice_flops(fix[a:b], (256, 256), 32), float(b - a)], dtype=torch.float64)
+        dist.all_reduce(mine)                      # test-only: the data path has no collective
+        if rank == 0:
+            q.put(dict(sum=float(mine[0]), frames=int(mine[1]),
+                       whole=_slice_flops(fix, (256, 256), 32)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_account_for_the_whole_batch_work():
+    """Each rank plans and costs ITS slice of one fixed batch (BASELINE config 4's fixations);
+    the per-rank algorithmic FLOPs add up to the whole batch's exactly: frames are independent,
+    and a rank's roofline numerator is its slice's."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    n = 37
+    mp.spawn(_cost_worker, args=(2, _free_port(), n, q), nprocs=2, join=True)
+    got = q.get()
+    assert got["frames"] == n
+    assert got["sum"] == got["whole"] > 0
+
+
 def test_bench_fixation_track_stays_inside_the_frame():
     import bench
 

@@ -130,36 +130,3 @@ def test_frame_request_graph_equals_foveate_float32_and_reports_plan():
     finally:
         req.close()
         plan.close()
-
-
-def test_harness_config_validation_matches_reference():
-    # bench.py:48-56: warm-up >= 3, iterations >= 10, no empty axes
-    from paper_2012_08655_b200 import harness
-    img = fk.RasterImage.from_array(np.zeros((64, 64, 3), np.uint8))
-    with pytest.raises(ValueError, match="warmup"):
-        harness.BenchConfig(images=(img,), warmup=2)
-    with pytest.raises(ValueError, match="iterations"):
-        harness.BenchConfig(images=(img,), iterations=5)
-    with pytest.raises(ValueError, match="empty"):
-        harness.BenchConfig(images=())
-    assert harness.CSV_COLUMNS[:4] == ["method", "image_w", "image_h", "fragment"]
-    with pytest.raises(ValueError, match="unknown method"):
-        harness.run_benchmark(harness.BenchConfig(images=(img,), methods=("pyramid",)))
-
-
-@pytest.mark.gpu
-def test_harness_rows_and_csv(tmp_path):
-    from paper_2012_08655_b200 import harness
-    rng = np.random.default_rng(11)
-    img = fk.RasterImage.from_array(rng.integers(0, 256, (270, 480, 3), dtype=np.uint8))
-    cfg = harness.BenchConfig(images=(img,), fragments=(16, 32), e_corners=(20.0, 60.0),
-                              fixations=("center", "corner", (100, 50)))
-    rows = harness.run_benchmark(cfg)
-    assert len(rows) == 2 * 2 * 3 and all(set(r) == set(harness.CSV_COLUMNS) for r in rows)
-    assert [r["fragment"] for r in rows[:6]] == [16] * 6          # the reference's sweep order
-    assert rows[1]["fixation_x"] == 0.0 and rows[2]["fixation_x"] == 100.0
-    # stronger foveation -> at least as many regions and taps (test_acceptance.py:208-248 trends)
-    assert rows[3]["max_filter"] >= rows[0]["max_filter"]
-    harness.write_csv(rows, tmp_path / "b.csv")
-    head = (tmp_path / "b.csv").read_text().splitlines()[0]
-    assert head == ",".join(harness.CSV_COLUMNS)
