@@ -165,6 +165,49 @@ __global__ void __launch_bounds__(128, 3) k_new(proto_args a, const float *taps)
     if (sink == 0x12345u) a.sink[blockIdx.x] = sink;
 }
 
+// ---- mode 2: H pass only, one row x 48 columns per lane (64-pixel strips, 4 warps x 48 columns)
+__global__ void __launch_bounds__(128, 2) k_h48(proto_args a, const float *taps)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const int L = a.L;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int a0 = a.skew + 48 * warp;
+    const int d = a0 & 15, zf = d / 3, rem = d - 3 * zf;
+    const int nchunk_h = (zf + L + 3) >> 2;
+    const int nch_max = (5 + L + 3) >> 2;
+    const int nq = (15 + 144 + 48 + 12 * nch_max + 64 + 15) / 16;
+    const int ipitch = 68;
+    unsigned char *raw = sm;
+    float *wh = reinterpret_cast<float *>(sm + nq * kQS2);
+    float *ring = wh + kWarps * (4 * nch_max + 4);
+    for (int i = tid; i < nq * kQS2; i += 128) {
+        const int ch = i >> 10, row = (i >> 4) & 63, b = i & 15;
+        raw[i] = src_byte(row & 31, ch * 16 + b);
+    }
+    {
+        float *w = wh + warp * (4 * nch_max + 4);
+        for (int i = lane; i < 4 * nchunk_h + 4; i += 32) w[i] = i >= zf && i < zf + L ? taps[i - zf] * kTapScaleH : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t raw_s = smem_u32(raw);
+    const uint32_t wh_s = smem_u32(wh + warp * (4 * nch_max + 4));
+    unsigned sink = 0;
+    for (int it = 0; it < a.iters; it++) {
+        for (int half = 0; half < 2; half++) {
+            float h[48];
+            const uint32_t rowA = raw_s + (uint32_t)((a0 >> 4) * kQS2 + (lane + 32 * half) * kQB);
+            h_bytes48(rowA, (uint32_t)rem * 8u, wh_s, nchunk_h, h);
+            float *rp = ring + (size_t)(48 * warp) * ipitch + lane + 32 * half;
+#pragma unroll
+            for (int j = 0; j < 48; j++) rp[j * ipitch] = h[j];
+            if (a.hout && it == a.iters - 1)
+                for (int j = 0; j < 48; j++) a.hout[(lane + 32 * half) * 192 + 48 * warp + j] = h[j];
+        }
+        __syncwarp();
+    }
+    if (sink == 0x12345u) a.sink[blockIdx.x] = sink;
+}
+
 } // namespace
 
 static void reference(int L, int skew_bytes, const std::vector<float> &taps, int rows, int vrows,
@@ -284,6 +327,46 @@ int main(int argc, char **argv)
                 for (int i = 0; i < vrows * 96; i++) badv += memcmp(&vg[i], &vref[i], 4) != 0;
                 printf("L %3d skew %2d hv %d %s occ %d  %8.3f ms  %6.2f TFLOP/s %5.1f%%  H bad %ld  V bad %ld\n", L, skew, hv,
                        mode ? "wide " : "ffma ", occ, best, tf, 100 * tf / peak, badh, badv);
+                if (mode == 1 && hv == 1) { /* the 48-column H task, H only */
+                    const int nch_max = (5 + L + 3) >> 2;
+                    const int nq = (15 + 144 + 48 + 12 * nch_max + 64 + 15) / 16;
+                    const size_t sm48 = nq * kQS2 + (kWarps * (4 * nch_max + 4) + 192 * 68) * 4;
+                    float *h48;
+                    cudaMalloc(&h48, 64 * 192 * 4);
+                    proto_args a48{L, tile0, kIters, 1, h48, nullptr, sink};
+                    cudaFuncSetAttribute(k_h48, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm48);
+                    int occ48 = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ48, k_h48, 128, sm48);
+                    const int grid48 = p.multiProcessorCount * occ48;
+                    float best48 = 1e30f;
+                    for (int rep = 0; rep < 3; rep++) {
+                        cudaEventRecord(e0);
+                        k_h48<<<grid48, 128, sm48>>>(a48, dtaps);
+                        cudaEventRecord(e1);
+                        if (cudaEventSynchronize(e1) != cudaSuccess) { printf("h48 launch failed\n"); return 1; }
+                        float ms;
+                        cudaEventElapsedTime(&ms, e0, e1);
+                        best48 = ms < best48 ? ms : best48;
+                    }
+                    const double tf48 = 2.0 * 64.0 * 192 * L * kIters * grid48 / (best48 * 1e-3) / 1e12;
+                    std::vector<float> hg48(64 * 192);
+                    cudaMemcpy(hg48.data(), h48, hg48.size() * 4, cudaMemcpyDeviceToHost);
+                    long bad48 = 0; /* reference: 192 columns of the same byte stream */
+                    for (int row = 0; row < 64; row++)
+                        for (int c2 = 0; c2 < 192; c2++) {
+                            float acc = 0.f;
+                            for (int k2 = 0; k2 < L; k2++) {
+                                const float x = ldexpf((float)src_byte(row & 31, tile0 + c2 + 3 * k2), -133);
+                                const float g = taps[k2] * kTapScaleH;
+                                acc = k2 == 0 ? g * x : fmaf(g, x, acc);
+                            }
+                            bad48 += memcmp(&acc, &hg48[row * 192 + c2], 4) != 0;
+                        }
+                    printf("L %3d skew %2d hv 1 h48   occ %d  %8.3f ms  %6.2f TFLOP/s %5.1f%%  H bad %ld\n", L, skew, occ48,
+                           best48, tf48, 100 * tf48 / peak, bad48);
+                    cudaFree(h48);
+                }
+
             }
         }
     return 0;

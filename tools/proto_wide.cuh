@@ -154,6 +154,96 @@ __device__ __forceinline__ void h_bytes2(uint32_t rowA, uint32_t rowB, uint32_t 
 }
 
 /*
+ * Horizontal task on raw bytes, ONE row x 48 float columns (16 pixels): acc[j] = sum_k g[k] *
+ * A[j + 3k], j in [0, 48).  Same stream conventions as h_bytes2.  Window: ring of eight slots
+ * of 12 floats (a chunk of four taps reads 48 + 9 floats = five slots, the sixth is converted
+ * for the next chunk; eight because the ring must turn with the quads: 2 turns = 8 chunks = 6
+ * quads).  A converted byte is used by up to 16 FMAs instead of 8.
+ */
+__device__ __forceinline__ void h_bytes48(uint32_t rowA, uint32_t bsh, uint32_t wts, int nchunk,
+                                          float (&acc)[48])
+{
+    float w[96];
+    auto cvt = [&](const int s, uint32_t a0, uint32_t a1) {
+        const uint32_t va = __funnelshift_r(a0, a1, bsh);
+        w[s + 0] = __uint_as_float(__byte_perm(va, 0u, 0x4044));
+        w[s + 1] = __uint_as_float(__byte_perm(va, 0u, 0x4144));
+        w[s + 2] = __uint_as_float(__byte_perm(va, 0u, 0x4244));
+        w[s + 3] = __uint_as_float(__byte_perm(va, 0u, 0x4344));
+    };
+    /* slots 0..4 = floats 0..59 = words 0..14 (+ word 15 for the shift): quads 0..3 */
+    uint4 q0 = lds128u(rowA), q1 = lds128u(rowA + kQS2), q2 = lds128u(rowA + 2 * kQS2),
+          q3 = lds128u(rowA + 3 * kQS2);
+    cvt(0, q0.x, q0.y); cvt(4, q0.y, q0.z); cvt(8, q0.z, q0.w); cvt(12, q0.w, q1.x);
+    cvt(16, q1.x, q1.y); cvt(20, q1.y, q1.z); cvt(24, q1.z, q1.w); cvt(28, q1.w, q2.x);
+    cvt(32, q2.x, q2.y); cvt(36, q2.y, q2.z); cvt(40, q2.z, q2.w); cvt(44, q2.w, q3.x);
+    cvt(48, q3.x, q3.y); cvt(52, q3.y, q3.z); cvt(56, q3.z, q3.w);
+    /* the stream from word 15 on, in quads: qa = words 12..15 (q3), qb = 16..19, qc = 20..23 */
+    uint4 qa = q3, qb = lds128u(rowA + 4 * kQS2), qc = qb;
+#pragma unroll
+    for (int j = 0; j < 48; j++) acc[j] = 0.0f;
+    uint32_t nA = rowA;
+    float4 g4 = lds128f(wts);
+    uint32_t wa = wts + 16;
+    auto fmas = [&](const int p, const float (&g)[4]) {
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+#pragma unroll
+            for (int j = 0; j < 48; j++) acc[j] = fmaf(g[t], w[(12 * p + 3 * t + j) % 96], acc[j]);
+    };
+    /* chunk c (phase p = c mod 8) converts slot p + 5 = floats 12 (c + 5) .. = words 15 + 3c ..
+     * 17 + 3c (+ 18 + 3c for the shift).  Word 15 + 3c lies in quad (15 + 3c) / 4: the word ->
+     * register map repeats every 4 chunks (3 quads), the slot map every 8. */
+    for (int c = 0; c < nchunk; c += 8) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) { /* two turns of four chunks */
+            const int p0 = 4 * h;
+            { /* words 15, 16, 17 (18): qa.w, qb.x, qb.y, (qb.z); load words 20..23 */
+                const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+                g4 = lds128f(wa);
+                qc = lds128u(nA + 5 * kQS2);
+                cvt((12 * (p0 + 5)) % 96 + 0, qa.w, qb.x);
+                cvt((12 * (p0 + 5)) % 96 + 4, qb.x, qb.y);
+                cvt((12 * (p0 + 5)) % 96 + 8, qb.y, qb.z);
+                fmas(p0, g);
+            }
+            if (c + p0 + 1 >= nchunk) return;
+            { /* words 18, 19, 20 (21): qb.z, qb.w, qc.x, (qc.y); load words 24..27 */
+                const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+                g4 = lds128f(wa + 16);
+                qa = lds128u(nA + 6 * kQS2);
+                cvt((12 * (p0 + 6)) % 96 + 0, qb.z, qb.w);
+                cvt((12 * (p0 + 6)) % 96 + 4, qb.w, qc.x);
+                cvt((12 * (p0 + 6)) % 96 + 8, qc.x, qc.y);
+                fmas(p0 + 1, g);
+            }
+            if (c + p0 + 2 >= nchunk) return;
+            { /* words 21, 22, 23 (24): qc.y, qc.z, qc.w, (qa.x); load words 28..31 */
+                const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+                g4 = lds128f(wa + 32);
+                qb = lds128u(nA + 7 * kQS2);
+                cvt((12 * (p0 + 7)) % 96 + 0, qc.y, qc.z);
+                cvt((12 * (p0 + 7)) % 96 + 4, qc.z, qc.w);
+                cvt((12 * (p0 + 7)) % 96 + 8, qc.w, qa.x);
+                fmas(p0 + 2, g);
+            }
+            if (c + p0 + 3 >= nchunk) return;
+            { /* words 24, 25, 26 (27): qa.x, qa.y, qa.z, (qa.w); no load */
+                const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+                g4 = lds128f(wa + 48);
+                wa += 64;
+                cvt((12 * (p0 + 8)) % 96 + 0, qa.x, qa.y);
+                cvt((12 * (p0 + 8)) % 96 + 4, qa.y, qa.z);
+                cvt((12 * (p0 + 8)) % 96 + 8, qa.z, qa.w);
+                nA += 3 * kQS2;
+                fmas(p0 + 3, g);
+            }
+            if (c + p0 + 4 >= nchunk) return;
+        }
+    }
+}
+
+/*
  * Vertical task on the transposed intermediate: acc[j][k] = sum_t g[t] * col_k[row0 + j + t],
  * j < 16 output rows, k < 3 adjacent columns (one RGB pixel).  `col` = shared address of row 0
  * of the first column, `cpitch` bytes between columns; a column is a ring of `cap` rows; row0
