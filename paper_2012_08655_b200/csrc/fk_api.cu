@@ -378,6 +378,7 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     p->custom = 0;
     /* a request's plan (fk_request_create) zeroes its counters in the plan kernel and reports
      * to pinned host memory: no memset and no copy nodes in the captured graph */
+    p->d.canonical = 1;
     p->d.self_zero = p->request_info != nullptr && n_frames == 1;
     p->d.info_out = n_frames == 1 ? p->request_info : nullptr;
     if (!p->d.self_zero)
@@ -451,6 +452,7 @@ int fk_plan_density(fk_plan *p, const fk_params *prm, int n_frames, const double
     const fk_density_dev den = {p->density_map, map_w, map_h, sigma_max};
     p->d.strip_rows = fk_strip_rows_for(n_frames);
     p->d.mixed = h->no_mixed ? 0 : 1;
+    p->d.canonical = 1;
     p->d.self_zero = 0;
     p->d.info_out = nullptr;
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, den, s));
@@ -514,6 +516,7 @@ int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     p->d.strip_rows = fk_strip_rows_for(1);
     p->d.mixed = 0; /* a caller's bank: tap offsets are not the canonical r * r */
+    p->d.canonical = 0;
     p->d.self_zero = 0;
     p->d.info_out = nullptr;
     FK_CUDA(h, fk_launch_order(p->d, 1, s));

@@ -106,6 +106,7 @@ struct fk_plan_dev {
     int nsub_y;          /* strips per fragment down: ceil(fragment / FK_STRIP_ROWS) */
     int strip_rows;      /* tallest strip the plan kernel merges fragments into (fk_strip_rows_for) */
     int mixed;           /* emit mixed items (FK_ITEM_MIXED) for groups of cells that differ */
+    int canonical;       /* taps are the canonical table: the filter of radius r starts at r * r */
     int self_zero;       /* one-frame plans: the plan kernel zeroes `counters` itself (no memset node) */
     int32_t *info_out;   /* optional host-mapped words the plan kernel fills for frame 0:
                             [0, 8) meta, [8] rejected fixations, [16, 16 + cells) tap counts */

@@ -68,11 +68,19 @@ __device__ __forceinline__ int fk_cell_of(int extent, int F, int off, int n, lon
  * way (a 64-pixel fragment is two columns, each the head of its own strips), and only
  * fragments taller than FK_STRIP_ROWS are cut into pieces without merging.
  */
-__device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const int32_t *len,
-                              const int32_t *off, int32_t *strip)
+template <typename CT>
+__device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT *len,
+                              const int32_t *off_global, CT *strip)
 {
-    /* len / off / strip: the frame's cell arrays -- the CTA's shared-memory copies when they
-     * fit (the walks below are chains of dependent loads), else the plan's global arrays */
+    /* len / strip: the frame's cell arrays -- 16-bit copies in the CTA's shared memory when they
+     * fit (the walks below are chains of dependent loads), else the plan's global arrays.
+     * off_global: the tap offsets of a caller's bank (fk_plan_set_grid), nullptr for the
+     * canonical table, where the taps of radius r start at r * r. */
+    auto off_of = [&](int c) -> int {
+        if (off_global) return off_global[c];
+        const int r = ((int)len[c] - 1) >> 1;
+        return r * r;
+    };
     __shared__ int ccount[FK_NCLASS];
     __shared__ int cbase[FK_NCLASS];
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -100,14 +108,14 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const in
         const int g0 = lead + ((gx - lead) / mgrp) * mgrp;
         const int g1 = g0 + mgrp < gw ? g0 + mgrp : gw;
         if (g1 - g0 < 2) return 0;
-        const int32_t *lr = len + gy * gw, *orow = off + gy * gw;
-        const int L0 = lr[g0], o0 = orow[g0];
+        const CT *lr = len + gy * gw;
+        const int L0 = lr[g0], o0 = off_of(gy * gw + g0);
         bool same = true;
         int lmax = 0;
         for (int x = g0; x < g1; x++) {
             if (lr[x] <= 1) return 0;
-            same = same && lr[x] == L0 && orow[x] == o0;
-            lmax = lr[x] > lmax ? lr[x] : lmax;
+            same = same && lr[x] == L0 && off_of(gy * gw + x) == o0;
+            lmax = lr[x] > lmax ? (int)lr[x] : lmax;
         }
         /* a warp's 8 pixel columns must lie in one cell: F = 8 or 16 */
         if (!same && (!pd.mixed || (F & 7) != 0 || lmax > FK_CLASS_L4)) return 0;
@@ -133,7 +141,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const in
             bool joins = mergeable && head >= 0 && gy - head < maxc && u0 == hu0 && u1 == hu1 &&
                          kind == hkind;
             for (int x = u0; joins && x < u1; x++) /* the same filter(s) as the head row */
-                joins = len[gy * gw + x] == len[head * gw + x] && off[gy * gw + x] == off[head * gw + x];
+                joins = len[gy * gw + x] == len[head * gw + x] && off_of(gy * gw + x) == off_of(head * gw + x);
             if (joins) {
                 strip[c] = 0;
                 strip[head * gw + gx] += 1;
@@ -162,7 +170,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const in
      * unit lies in cell u0 + 8 w / F (every cell of a group but the last is F wide) */
     auto unit_filters = [&](int c, int u0, int u1, int kind, int &lmax, uint32_t &toff) {
         lmax = len[c];
-        toff = (uint32_t)off[c];
+        toff = (uint32_t)off_of(c);
         if (kind != 2) return;
         const int gy = c / gw;
         toff = FK_ITEM_MIXED;
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(FK_PLAN_THREADS_MAX)
 fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, int n_frames,
                fk_density_dev den, int cells_in_smem)
 {
-    extern __shared__ int32_t sm_cells[]; /* [3][cap]: length, offset, strip (cells_in_smem) */
+    extern __shared__ int16_t sm_cells[]; /* [2][cap]: length, strip (cells_in_smem) */
     __shared__ int s_lmax;
     const int f = blockIdx.x;
     if (f >= n_frames) return;
@@ -309,9 +317,6 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
     int32_t *raw = pd.raw_length + (size_t)f * pd.cap;
     int32_t *len = pd.length + (size_t)f * pd.cap;
     int32_t *off = pd.offset + (size_t)f * pd.cap;
-    int32_t *len_s = cells_in_smem ? sm_cells : len;
-    int32_t *off_s = cells_in_smem ? sm_cells + pd.cap : off;
-    int32_t *strip_s = cells_in_smem ? sm_cells + 2 * pd.cap : pd.strip + (size_t)f * pd.cap;
     int lmax = 1;
     for (int c = tid; c < ncells; c += blockDim.x) {
         const int gy = c / gw, gx = c - gy * gw;
@@ -359,10 +364,7 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
         len[c] = L;
         const int r = (L - 1) >> 1;
         off[c] = r * r;
-        if (cells_in_smem) {
-            len_s[c] = L;
-            off_s[c] = r * r;
-        }
+        if (cells_in_smem) sm_cells[c] = (int16_t)(L < 32767 ? L : 32767);
         lmax = L > lmax ? L : lmax;
     }
     atomicMax(&s_lmax, lmax);
@@ -381,9 +383,14 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
     if (pd.info_out && f == 0) { /* the request's plan summary, straight into pinned host memory */
         if (tid < FK_META_WORDS) pd.info_out[tid] = meta[tid];
         if (tid == FK_META_WORDS) pd.info_out[tid] = 0;
-        for (int c = tid; c < ncells; c += blockDim.x) pd.info_out[16 + c] = len_s[c];
+        for (int c = tid; c < ncells; c += blockDim.x) pd.info_out[16 + c] = len[c];
     }
-    fk_emit_items(pd, f, ncells, len_s, off_s, strip_s);
+    /* filters the fast kernels cannot take anyway (> 8191 taps are rejected by the host) never
+     * reach 16 bits; the model's offsets are the canonical r * r */
+    if (cells_in_smem)
+        fk_emit_items<int16_t>(pd, f, ncells, sm_cells, nullptr, sm_cells + pd.cap);
+    else
+        fk_emit_items<int32_t>(pd, f, ncells, len, nullptr, pd.strip + (size_t)f * pd.cap);
 }
 
 /* Item emission from the cell arrays of a plan: a caller-supplied grid (fk_plan_set_grid), or
@@ -391,7 +398,7 @@ fk_plan_kernel(fk_plan_dev pd, fk_params prm, const double *__restrict__ fix, in
 __global__ void __launch_bounds__(FK_PLAN_THREADS_MAX)
 fk_order_kernel(fk_plan_dev pd, int n_frames, int cells_in_smem)
 {
-    extern __shared__ int32_t sm_cells[];
+    extern __shared__ int16_t sm_cells[];
     const int f = blockIdx.x;
     if (f >= n_frames) return;
     const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
@@ -400,19 +407,16 @@ fk_order_kernel(fk_plan_dev pd, int n_frames, int cells_in_smem)
         return;
     }
     const int ncells = meta[FK_META_GW] * meta[FK_META_GH];
-    const int32_t *len = pd.length + (size_t)f * pd.cap, *off = pd.offset + (size_t)f * pd.cap;
-    int32_t *strip = pd.strip + (size_t)f * pd.cap;
+    const int32_t *len = pd.length + (size_t)f * pd.cap;
+    const int32_t *off = pd.canonical ? nullptr : pd.offset + (size_t)f * pd.cap;
     if (cells_in_smem) {
-        for (int c = threadIdx.x; c < ncells; c += blockDim.x) {
-            sm_cells[c] = len[c];
-            sm_cells[pd.cap + c] = off[c];
-        }
+        for (int c = threadIdx.x; c < ncells; c += blockDim.x)
+            sm_cells[c] = (int16_t)(len[c] < 32767 ? len[c] : 32767);
         __syncthreads();
-        len = sm_cells;
-        off = sm_cells + pd.cap;
-        strip = sm_cells + 2 * pd.cap;
+        fk_emit_items<int16_t>(pd, f, ncells, sm_cells, off, sm_cells + pd.cap);
+    } else {
+        fk_emit_items<int32_t>(pd, f, ncells, len, off, pd.strip + (size_t)f * pd.cap);
     }
-    fk_emit_items(pd, f, ncells, len, off, strip);
 }
 
 /* filters.py:30-38 at sigma = L/6 (filters.py:78): one CTA per odd length. */
@@ -460,12 +464,28 @@ cudaError_t fk_launch_build_lut(double *lut64, float *lut32, int max_length, cud
     return cudaGetLastError();
 }
 
+/* One CTA per frame: large CTAs while all frames fit the device in one wave (a streaming request
+ * plans one frame, the headline batch 256: the cell loop is a chain of fp64 divisions per cell
+ * and the emission walks are short, so threads are what shortens it), small ones for big
+ * batches. */
+static int plan_threads(int n_frames)
+{
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 1;
+    }
+    return n_frames <= 2 * sms ? FK_PLAN_THREADS_MAX : FK_PLAN_THREADS;
+}
+
 /* Dynamic shared memory for a frame's cell arrays (length, offset, strip), 0 when they do not
  * fit: the kernels then walk the plan's global arrays. */
 static size_t cell_smem_bytes(const fk_plan_dev &pd)
 {
-    const size_t need = 3 * (size_t)pd.cap * sizeof(int32_t);
-    return need <= 160 * 1024 ? need : 0;
+    const size_t need = 2 * (size_t)pd.cap * sizeof(int16_t); /* tap counts and strip heights */
+    return need <= 200 * 1024 ? need : 0;
 }
 
 cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_frames,
@@ -476,9 +496,7 @@ cudaError_t fk_launch_plan(const fk_plan_dev &pd, const fk_params &prm, int n_fr
         cudaError_t e = cudaFuncSetAttribute(fk_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    /* a handful of frames (a streaming request plans one): one large CTA per frame, the cell
-     * loop is a chain of fp64 divisions per cell and nothing else runs beside it */
-    const int threads = n_frames <= 16 ? FK_PLAN_THREADS_MAX : FK_PLAN_THREADS;
+    const int threads = plan_threads(n_frames);
     fk_plan_kernel<<<n_frames, threads, smem, s>>>(pd, prm, fix_dev, n_frames, den, smem != 0);
     return cudaGetLastError();
 }
@@ -490,6 +508,6 @@ cudaError_t fk_launch_order(const fk_plan_dev &pd, int n_frames, cudaStream_t s)
         cudaError_t e = cudaFuncSetAttribute(fk_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    fk_order_kernel<<<n_frames, n_frames <= 16 ? FK_PLAN_THREADS_MAX : FK_PLAN_THREADS, smem, s>>>(pd, n_frames, smem != 0);
+    fk_order_kernel<<<n_frames, plan_threads(n_frames), smem, s>>>(pd, n_frames, smem != 0);
     return cudaGetLastError();
 }
