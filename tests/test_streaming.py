@@ -130,3 +130,17 @@ def test_frame_request_graph_equals_foveate_float32_and_reports_plan():
     finally:
         req.close()
         plan.close()
+
+
+@pytest.mark.gpu
+def test_stream_single_channel_image():
+    """Gray sources go through the row-partitioned kernel inside the request graph."""
+    rng = np.random.default_rng(12)
+    img = rng.integers(0, 256, (200, 300), dtype=np.uint8)
+    with FoveationStream(img, fk.FoveationParams(fragment_size=32)) as s:
+        for (x, y) in [(150.0, 100.0), (299.0, 0.0)]:
+            s.submit(x, y)
+            out, stats = s.get(timeout=30)
+            ref, *_ = fk.foveate(fk.RasterImage.from_array(img),
+                                 fk.FoveationParams(fragment_size=32, fixation=(x, y)))
+            assert out.shape == (200, 300, 1) and np.array_equal(out, ref.data)
