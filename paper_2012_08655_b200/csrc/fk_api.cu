@@ -590,14 +590,29 @@ int fk_plan_read_items(fk_plan *p, int klass, uint32_t *items_host, int capacity
         return fk_fail(h, FK_EINVAL, "class %d outside [0, %d)", klass, FK_NCLASS);
     FK_CUDA(h, cudaSetDevice(h->device));
     FK_CUDA(h, cudaStreamSynchronize(as_stream(stream)));
-    int32_t n = 0;
-    FK_CUDA(h, cudaMemcpy(&n, p->d.counters + klass, sizeof n, cudaMemcpyDeviceToHost));
-    *count = n;
+    /* a list has two ends (fk_class_list): tall strips at the front of its region, short ones
+     * at the back; they are returned front first, in the order the render draws them */
+    int32_t nf = 0, nb = 0;
+    FK_CUDA(h, cudaMemcpy(&nf, p->d.counters + klass, sizeof nf, cudaMemcpyDeviceToHost));
+    FK_CUDA(h, cudaMemcpy(&nb, p->d.counters + FK_COUNTER_BACK + klass, sizeof nb,
+                          cudaMemcpyDeviceToHost));
+    *count = nf + nb;
     if (!items_host || capacity <= 0) return FK_OK;
-    const int take = n < capacity ? n : capacity;
-    if (take > 0)
-        FK_CUDA(h, cudaMemcpy(items_host, p->d.items + (size_t)klass * p->d.items_cap,
-                              (size_t)take * sizeof(fk_item), cudaMemcpyDeviceToHost));
+    const fk_item *base = p->d.items + (size_t)klass * p->d.items_cap;
+    fk_item *dst = reinterpret_cast<fk_item *>(items_host);
+    const int take_f = nf < capacity ? nf : capacity;
+    if (take_f > 0)
+        FK_CUDA(h, cudaMemcpy(dst, base, (size_t)take_f * sizeof(fk_item), cudaMemcpyDeviceToHost));
+    const int take_b = nb < capacity - take_f ? nb : capacity - take_f;
+    if (take_b > 0) {
+        FK_CUDA(h, cudaMemcpy(dst + take_f, base + (p->d.items_cap - (size_t)take_b),
+                              (size_t)take_b * sizeof(fk_item), cudaMemcpyDeviceToHost));
+        for (int i = 0, j = take_b - 1; i < j; i++, j--) { /* drawn from the end downwards */
+            const fk_item t = dst[take_f + i];
+            dst[take_f + i] = dst[take_f + j];
+            dst[take_f + j] = t;
+        }
+    }
     return FK_OK;
 }
 
@@ -636,7 +651,7 @@ static int fk_render_any(fk_handle *h, const fk_plan *p, const void *in, void *o
          * so the plan's work lists are emitted once more without them (the cell arrays stay) */
         fk_plan *pm = const_cast<fk_plan *>(p);
         pm->d.mixed = 0;
-        FK_CUDA(h, cudaMemsetAsync(pm->d.counters, 0, 2 * FK_NCLASS * sizeof(int32_t),
+        FK_CUDA(h, cudaMemsetAsync(pm->d.counters, 0, FK_COUNTER_BAD * sizeof(int32_t),
                                    as_stream(stream)));
         FK_CUDA(h, fk_launch_order(pm->d, n_frames, as_stream(stream)));
         launches++;

@@ -53,8 +53,8 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
     __shared__ int s_idx;
     float *wts = smem;
     float *interm = smem + w_floats;
-    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
-    const int n_items = pd.counters[klass];
+    const fk_class_list list = fk_list_of(pd, klass);
+    const int n_items = list.n_items;
     int *cursor = pd.counters + FK_NCLASS + klass;
     const int W = pd.width, H = pd.height;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -65,7 +65,7 @@ fk_blur_generic(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, i
         __syncthreads();
         const int idx = s_idx;
         if (idx >= n_items) break;
-        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(list.at(idx)));
         const int fw = (int)(q.z & 0xffu), fh_all = (int)(q.z >> 21);
         if (fw == 0 || fh_all == 0) continue;
         const int f = (int)q.x;
@@ -135,11 +135,11 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 fk_copy_items(fk_plan_dev pd, const T *__restrict__ in, T *__restrict__ out, int C)
 {
-    const fk_item *items = pd.items + (size_t)FK_CLASS_COPY * pd.items_cap;
-    const int n_items = pd.counters[FK_CLASS_COPY];
+    const fk_class_list list = fk_list_of(pd, FK_CLASS_COPY);
+    const int n_items = list.n_items;
     const int W = pd.width, H = pd.height;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(items + idx));
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(list.at(idx)));
         const int fw = (int)(q.z & 0xffu), fh = (int)(q.z >> 21);
         const int x0 = (int)(q.y & 0xffffu), y0 = (int)(q.y >> 16);
         const size_t frame_off = (size_t)q.x * H * W * C;

@@ -458,8 +458,8 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     const int W = pd.width, H = pd.height;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
-    const int n_items = pd.counters[klass];
+    const fk_class_list list = fk_list_of(pd, klass);
+    const int n_items = list.n_items;
     /* Items are dealt dynamically: a CTA starts with items blockIdx and blockIdx + grid and
      * draws every further one from the class's cursor (zeroed before the render launches)
      * when it starts an item, two items ahead of its use, so the draw, its hand-over through
@@ -468,7 +468,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     const int stride = (int)gridDim.x;
     const uint4 none = make_uint4(0u, 0u, 0u, 0u);
     auto load_item = [&](int i) {
-        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
+        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(list.at(i))) : none;
     };
     /* One 32-row block of an item.  Rows: the box origin is clamped into the image so that
      * every clamped source row of the block lies inside the box.  Columns: the box starts at
@@ -1057,18 +1057,23 @@ __device__ __forceinline__ uint32_t warp_taps_off(const uint4 q, int warp)
     return (q.w & FK_ITEM_MIXED) ? r * r : q.w;
 }
 /* First 16-byte unit of a row that the TMA box of an item fetches (g.r: the longest filter).
- * uint8: the chunk that holds the byte three pixels left of the tile -- every warp's stream
- * starts 3 zpad <= 9 bytes left of ITS tile, which starts at or right of the item's; float32:
- * the quad of the pixel at or below the tile's first that is a multiple of four (h_float). */
-template <typename T> __device__ __forceinline__ int box_unit(const item_geo &g)
+ * uint8: the chunk that holds the stream's first byte, 3 zpad bytes left of the tile -- in a
+ * plan that may hold mixed items, three pixels left of it: every warp's stream starts 3 zpad
+ * <= 9 bytes left of ITS tile, which starts at or right of the item's; float32: the quad of
+ * the pixel at or below the tile's first that is a multiple of four (h_float). */
+template <typename T, bool MIXED> __device__ __forceinline__ int box_unit(const item_geo &g)
 {
-    return sizeof(T) == 1 ? ((g.x0 - g.r - 3) * kC) >> 4 : (((g.x0 - g.r) & ~3) * kC) >> 2;
+    if (sizeof(T) != 1) return (((g.x0 - g.r) & ~3) * kC) >> 2;
+    const int lead_px = MIXED ? 3 : 4 * g.nchunk - g.L;
+    return ((g.x0 - g.r - lead_px) * kC) >> 4;
 }
 
 /* Three resident CTAs per SM with 167 registers beat four with 127 (27.0 k against 26.8 k
  * frames/s on the bench, 19.4 k against 18.8 k with corner fixations): at 127 the compiler
  * rematerialises addresses and constants inside the task set-up. */
-template <typename T, int MINB>
+/* MIXED: the plan may hold mixed items (fragments of 8 or 16 pixels); without them the per-warp
+ * geometry below folds into the item's at compile time. */
+template <typename T, int MINB, bool MIXED>
 __global__ void __launch_bounds__(kThreads, MINB)
 fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *__restrict__ in,
             T *__restrict__ out, int klass, int wts_floats, int nq, int icap, int ipitch, int nbuf)
@@ -1092,13 +1097,13 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
     const int W = pd.width, H = pd.height;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
-    const int n_items = pd.counters[klass];
+    const fk_class_list list = fk_list_of(pd, klass);
+    const int n_items = list.n_items;
     int *cursor = pd.counters + FK_NCLASS + klass;
     const int stride = (int)gridDim.x;
     const uint4 none = make_uint4(0u, 0u, 0u, 0u);
     auto load_item = [&](int i) {
-        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
+        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(list.at(i))) : none;
     };
     /* One 32-row block: the box starts at the 16-byte chunk that holds the tile's first byte
      * (possibly left of the image: TMA fills what is outside with zeros) and at the first
@@ -1106,13 +1111,13 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
     auto issue = [&](const item_geo &g, int rb, int buf) {
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
         mbar_expect_tx(bar + buf, (uint32_t)raw_bytes);
-        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, box_unit<T>(g), g.f);
+        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, box_unit<T, MIXED>(g), g.f);
     };
     auto fill_taps = [&](const uint4 q, int slot) {
-        const int L = warp_length(q, warp);
+        const int L = MIXED ? warp_length(q, warp) : (int)((q.z >> 8) & 0x1fffu);
         const int n = 4 * ((L + 3) >> 2) + 4;
         const int z = n - 4 - L; /* zeros in front (3 or 1), one zero quad behind */
-        const float *taps = pd.taps + warp_taps_off(q, warp);
+        const float *taps = pd.taps + (MIXED ? warp_taps_off(q, warp) : q.w);
         float *dst = wts + (warp * 3 + slot) * wts_floats;
         for (int i = lane; i < n; i += 32) {
             const int in_range = i >= z && i < z + L;
@@ -1192,7 +1197,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
         const item_geo g = decode_item<C>(q_cur, W);
         const int x0 = g.x0, y0 = g.y0, fw = g.fw, fh = g.fh, r = g.r;
         const int th = g.th, tw = g.tw;
-        const int rw = warp_radius(q_cur, warp), Lw = 2 * rw + 1, dw = r - rw;
+        const int rw = MIXED ? warp_radius(q_cur, warp) : r, Lw = 2 * rw + 1, dw = r - rw;
         const int nchunk = (Lw + 3) >> 2;
         const int zpad = 4 * nchunk - Lw;                  /* zeros in front of the taps: 3 or 1 */
         const int xw = x0 + 8 * warp - rw;                 /* first tile pixel of the warp's columns */
@@ -1210,7 +1215,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
             __syncwarp();
         }
         T *dst = out + (size_t)g.f * H * W * C;
-        const int box0 = box_unit<T>(g) * (kBytes ? 16 : 4); /* image element of the box's first */
+        const int box0 = box_unit<T, MIXED>(g) * (kBytes ? 16 : 4); /* image element of the box's first */
         /* the warp's stream (element 0 meets the first tap, padding included) inside the box */
         const int sw = (xw - zf) * C - box0;
         const int skew = (x0 - r) * C - box0;                      /* tile float 0 = raw element skew */
@@ -1492,7 +1497,8 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
     /* the intermediate: 2r rows the V pass still needs + the 32 of the next block.  A warp of
      * a mixed item whose filter is shorter than the item's longest is not aligned to the groups
      * of 8 output rows (up to 7 more rows wait for their group), hence 8 rows of slack */
-    const int icap = (2 * r + kTB + (pd.mixed ? 8 : 0) + 3) & ~3;
+    const bool mixed_items = pd.mixed && pd.fragment < FK_RECT && (pd.fragment & 7) == 0; /* fk_emit_items */
+    const int icap = (2 * r + kTB + (mixed_items ? 8 : 0) + 3) & ~3;
     const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
     size_t smem = (size_t)nq * kQStride + 128 +
                   ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
@@ -1507,7 +1513,8 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
     const size_t per_sm = h->prop.sharedMemPerMultiprocessor;
     const size_t reserved = h->prop.reservedSharedMemPerBlock;
     const bool two = 3 * (smem + reserved) > per_sm;
-    auto kernel = two ? fk_blur_tma<T, 2> : fk_blur_tma<T, 3>;
+    auto kernel = mixed_items ? (two ? fk_blur_tma<T, 2, true> : fk_blur_tma<T, 3, true>)
+                              : (two ? fk_blur_tma<T, 2, false> : fk_blur_tma<T, 3, false>);
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;

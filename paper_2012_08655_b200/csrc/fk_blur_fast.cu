@@ -72,12 +72,12 @@ fk_blur_fast(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     const int W = pd.width, H = pd.height;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const fk_item *items = pd.items + (size_t)klass * pd.items_cap;
-    const int n_items = pd.counters[klass];
+    const fk_class_list list = fk_list_of(pd, klass);
+    const int n_items = list.n_items;
     const int stride = (int)gridDim.x;
     const uint4 none = make_uint4(0u, 0u, 0u, 0u);
     auto load_item = [&](int i) {
-        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(items + i)) : none;
+        return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(list.at(i))) : none;
     };
 
     /* One 32-row block of an item: the box origin is clamped into the image so that every

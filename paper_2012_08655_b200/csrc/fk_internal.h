@@ -51,8 +51,13 @@ enum {
 #define FK_CLASS_L4 127
 #define FK_CLASS_GENERIC 5
 #define FK_CLASS_COPY 6
-#define FK_COUNTER_WORDS (2 * FK_NCLASS + 1)
-#define FK_COUNTER_BAD (2 * FK_NCLASS)
+/* counters: [0, N) items at the FRONT of each class list, [N, 2N) render cursors, [2N, 3N) items
+ * at the BACK of each list, [3N] frames whose fixation lies outside the image */
+#define FK_COUNTER_BACK (2 * FK_NCLASS)
+#define FK_COUNTER_BAD (3 * FK_NCLASS)
+#define FK_COUNTER_WORDS (3 * FK_NCLASS + 1)
+/* strips taller than this many rows go to the front of their list (fk_class_list) */
+#define FK_TALL_ROWS(L) ((L) <= FK_CLASS_L2 ? 64 : 128)
 
 static __host__ __device__ __forceinline__ int fk_class_of(int L)
 {
@@ -112,8 +117,7 @@ struct fk_plan_dev {
                             [0, 8) meta, [8] rejected fixations, [16, 16 + cells) tap counts */
     size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */
     fk_item *items;      /* [FK_NCLASS][items_cap] */
-    int32_t *counters;   /* [0, NCLASS): item counts; [NCLASS, 2 NCLASS): render cursors;
-                            [2 NCLASS]: frames whose fixation lies outside the image */
+    int32_t *counters;   /* FK_COUNTER_WORDS words, see FK_COUNTER_BACK */
     double *sigma;       /* [frames][cap] */
     int32_t *raw_length; /* [frames][cap] */
     int32_t *length;     /* [frames][cap], foveal cell forced to 1 */
@@ -123,6 +127,37 @@ struct fk_plan_dev {
     int32_t *meta;       /* [frames][FK_META_WORDS] */
     const float *taps;   /* fp32 tap table the offsets index (canonical LUT or custom) */
 };
+
+/*
+ * A class list has two ends.  The persistent CTAs of a render draw items in list order, so the
+ * items drawn last decide how long the launch's tail is: the plan kernel puts the TALL strips
+ * of every frame at the front of the list's region and the short ones at its back (filled
+ * downwards from items_cap - 1), and item i of the list is front[i] for i < n_front, else
+ * back[i - n_front] counted from the end.  Tall first is within 1-4 % of longest-processing-time
+ * order on the bench workloads (tools/strip_model.py), against 3-19 % for frame order.
+ */
+struct fk_class_list {
+    const fk_item *base;
+    size_t last; /* items_cap - 1 */
+    int n_front, n_items;
+#ifdef __CUDACC__
+    __device__ __forceinline__ const fk_item *at(int i) const
+    {
+        return i < n_front ? base + i : base + (last - (size_t)(i - n_front));
+    }
+#endif
+};
+#ifdef __CUDACC__
+static __device__ __forceinline__ fk_class_list fk_list_of(const fk_plan_dev &pd, int klass)
+{
+    fk_class_list l;
+    l.base = pd.items + (size_t)klass * pd.items_cap;
+    l.last = pd.items_cap - 1;
+    l.n_front = pd.counters[klass];
+    l.n_items = l.n_front + pd.counters[FK_COUNTER_BACK + klass];
+    return l;
+}
+#endif
 
 /* Density-map source of the sigma field (map == nullptr: retinal model). */
 struct fk_density_dev {

@@ -12,6 +12,8 @@
  * blockwise.py:107-133.  The operation order of SURVEY.md Appendix A is kept, and every
  * fp64 operation is an explicitly rounded intrinsic so nothing is fused.
  */
+#include <cstdlib>
+
 #include "fk_hypot.h"
 #include "fk_internal.h"
 
@@ -81,8 +83,8 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
         const int r = ((int)len[c] - 1) >> 1;
         return r * r;
     };
-    __shared__ int ccount[FK_NCLASS];
-    __shared__ int cbase[FK_NCLASS];
+    __shared__ int ccount[2 * FK_NCLASS]; /* [0, N): front of the class lists, [N, 2N): back */
+    __shared__ int cbase[2 * FK_NCLASS];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int32_t *meta = pd.meta + (size_t)f * FK_META_WORDS;
     const int sx = meta[FK_META_SX], sy = meta[FK_META_SY];
@@ -94,7 +96,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
     const int mgrp = merge ? FK_RECT / F : 1; /* cells per horizontal unit */
     const int lead = sx > 0 ? 1 : 0;
     const int per_cell = pd.nsub_x * pd.nsub_y; /* FK_RECT-wide columns of a wider fragment */
-    if (tid < FK_NCLASS) ccount[tid] = 0;
+    if (tid < 2 * FK_NCLASS) ccount[tid] = 0;
     __syncthreads();
 
     /* The unit [u0, u1) of grid row gy that contains cell gx, and its kind -- 0: the cell
@@ -203,19 +205,27 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
         return fw > 0 && fh > 0;
     };
 
+    /* which end of its class list a strip goes to (fk_class_list, fk_internal.h): tall strips to
+     * the front, so that the items the persistent CTAs draw last are short ones */
+    auto list_end = [&](int L, int fh) { return L > 1 && fh <= FK_TALL_ROWS(L) ? FK_NCLASS : 0; };
     for (int c = tid; c < ncells; c += nt) {
         int u0, u1, kind, lmax;
         uint32_t toff;
         const int n = strip_of(c, u0, u1, kind);
         if (n == 0) continue;
         unit_filters(c, u0, u1, kind, lmax, toff);
-        int cnt = 0, a, b2, w, h2;
-        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, u1, s, a, b2, w, h2) ? 1 : 0;
-        if (cnt) atomicAdd(&ccount[fk_class_of(lmax)], cnt);
+        int cnt = 0, a, b2, w, h2 = 0, hh = 0;
+        for (int s = 0; s < per_cell; s++)
+            if (sub_rect(c, n, u1, s, a, b2, w, h2)) {
+                cnt++;
+                hh = h2;
+            }
+        if (cnt) atomicAdd(&ccount[list_end(lmax, hh) + fk_class_of(lmax)], cnt);
     }
     __syncthreads();
-    if (tid < FK_NCLASS) { /* one reservation per class keeps a frame's items contiguous */
-        cbase[tid] = ccount[tid] ? atomicAdd(&pd.counters[tid], ccount[tid]) : 0;
+    if (tid < 2 * FK_NCLASS) { /* one reservation per class and end keeps a frame's items together */
+        const int k = tid < FK_NCLASS ? tid : FK_COUNTER_BACK + tid - FK_NCLASS;
+        cbase[tid] = ccount[tid] ? atomicAdd(&pd.counters[k], ccount[tid]) : 0;
         ccount[tid] = 0; /* becomes the running slot inside the reservation */
     }
     __syncthreads();
@@ -226,10 +236,18 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
         if (n == 0) continue;
         unit_filters(c, u0, u1, kind, L, toff);
         const int k = fk_class_of(L);
-        int cnt = 0, rx0, ry0, fw, fh;
-        for (int s = 0; s < per_cell; s++) cnt += sub_rect(c, n, u1, s, rx0, ry0, fw, fh) ? 1 : 0;
+        int cnt = 0, rx0, ry0, fw, fh = 0, hh = 0;
+        for (int s = 0; s < per_cell; s++)
+            if (sub_rect(c, n, u1, s, rx0, ry0, fw, fh)) {
+                cnt++;
+                hh = fh;
+            }
         if (cnt == 0) continue;
-        fk_item *dst = pd.items + (size_t)k * pd.items_cap + cbase[k] + atomicAdd(&ccount[k], cnt);
+        const int end = list_end(L, hh);
+        const int slot = cbase[end + k] + atomicAdd(&ccount[end + k], cnt);
+        fk_item *base = pd.items + (size_t)k * pd.items_cap;
+        /* front: upwards from 0; back: downwards from items_cap - 1 */
+        fk_item *dst = end ? base + (pd.items_cap - 1 - (size_t)slot) : base + slot;
         for (int s = 0; s < per_cell; s++) {
             if (!sub_rect(c, n, u1, s, rx0, ry0, fw, fh)) continue;
             fk_item it;
@@ -237,7 +255,8 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
             it.xy = (uint32_t)rx0 | ((uint32_t)ry0 << 16);
             it.geom = (uint32_t)fw | ((uint32_t)L << 8) | ((uint32_t)fh << 21);
             it.taps_off = toff;
-            *dst++ = it;
+            *dst = it;
+            dst += end ? -1 : 1;
         }
     }
 }
@@ -477,6 +496,8 @@ static int plan_threads(int n_frames)
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
             sms = 1;
     }
+    static const int force = getenv("FK_PLAN_THREADS") ? atoi(getenv("FK_PLAN_THREADS")) : 0;
+    if (force) return force;
     return n_frames <= 2 * sms ? FK_PLAN_THREADS_MAX : FK_PLAN_THREADS;
 }
 
