@@ -8,6 +8,7 @@ FK_ECUDA which surfaces here as ``RuntimeError``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 
 from . import _build
@@ -111,7 +112,8 @@ def lib():
     if _lib is None:
         with _lock:
             if _lib is None:
-                path = _build.build_native()
+                # FK_LIB_PATH (tuning runs): load an alternative build of libfovea.so as it is
+                path = os.environ.get("FK_LIB_PATH") or _build.build_native()
                 loaded = C.CDLL(str(path))
                 _declare(loaded)
                 if loaded.fk_abi_version() != 1:
