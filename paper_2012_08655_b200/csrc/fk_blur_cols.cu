@@ -1,8 +1,8 @@
 /*
  * fk_blur_cols.cu -- column-partitioned separable blur for RGB frames on sm_100a: fk_blur_cols
- * (float32 frames, and uint8 buffers TMA cannot describe) and, further down, fk_blur_bytes --
- * the hot kernel of the render path, uint8 frames by TMA -- which shares everything after the
- * H pass with it.
+ * (buffers TMA cannot describe) and, further down, fk_blur_tma -- the hot kernel of the render
+ * path, uint8 and float32 frames staged by TMA -- which shares everything after the H pass
+ * with it.
  *
  * Same arithmetic as blockwise.py:136-153 (_render_cell): clamp-to-edge tile, horizontal
  * pass over every tile row into a real-valued intermediate, vertical pass, one rounding
@@ -46,7 +46,7 @@
  * result does not change), and each panel costs one more pair of barriers.
  *
  * Taps are zero-padded to a multiple of 4 -- in FRONT for the V pass and for the H pass of
- * fk_blur_bytes, whose first chunk skips the zeros and starts from a plain product (see
+ * fk_blur_tma, whose first chunk skips the zeros and starts from a plain product (see
  * v_task_px), at the end for h_part; every shared-memory word a padded tap can touch holds a
  * finite value so 0 * garbage never produces a NaN.
  */
@@ -788,7 +788,8 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
 }
 
 /* =====================================================================================
- * fk_blur_bytes -- uint8 RGB frames: the H pass reads the TMA bytes directly.
+ * fk_blur_tma -- RGB frames staged by TMA: the H pass reads what landed directly (uint8 below;
+ * float32: h_float).
  *
  * No working tile, no conversion pass, no CTA barrier.  One 4-D TMA box per 32-row block,
  * over the batch seen as (16 bytes, rows, 16-byte chunks of a row, frames), lands the block
@@ -1570,7 +1571,7 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
         }
         return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
     }
-    /* uint8 by TMA: fk_blur_bytes, the kernel whose H pass reads the TMA bytes directly -- no
+    /* uint8 by TMA: fk_blur_tma, the kernel whose H pass reads the TMA bytes directly -- no
      * working tile, no conversion pass, no CTA barrier, 3 CTAs per SM up to 105 taps.  (Until the taps were padded in front it only won for the long filters.)
      * Variant 4: fk_blur_cols for every class, variant 5: same as the default. */
     if (h->variant == 5 || h->variant == 0 || h->variant == 6) { /* 6: one raw buffer (A/B runs) */

@@ -38,12 +38,13 @@ enum {
 #define FK_STRIP_ROWS 1024
 #define FK_NCLASS 7
 /* Classes 0..4 are rendered by the fast kernels, each launch with the shared-memory layout
- * of the class's longest filter.  uint8 frames staged by TMA: fk_blur_bytes (3 resident CTAs
- * per SM -- its register budget -- up to 89 taps, and up to 105 when the batch has nothing
- * longer; 2 up to 127).  Everything else (float32 frames, buffers TMA cannot describe): fk_blur_cols, 3
- * CTAs per SM in classes 0 and 1, 2 in classes 2 and 3 with a whole-width working tile and in
- * class 4 with the taps walked in panels.  Class 5 (longer filters) goes to the generic
- * kernel, class 6 holds the identity fragments (L = 1), plain copies. */
+ * of the class's longest filter.  Frames staged by TMA (uint8 and float32): fk_blur_tma, 3
+ * resident CTAs per SM -- its register budget -- while the layout fits three times (uint8: up
+ * to 105 taps; float32, whose raw blocks are four times the size: up to ~55), else 2.  Buffers
+ * TMA cannot describe: fk_blur_cols, 3 CTAs per SM in classes 0 and 1, 2 beyond, with the taps
+ * walked in panels in class 4.  Class 5 (longer filters) goes to the generic kernel, class 6
+ * holds the identity fragments (L = 1), plain copies.  (Merging classes 0-2 was measured:
+ * nothing on uint8, 3-22 % slower on float32.) */
 #define FK_CLASS_L0 23
 #define FK_CLASS_L1 47
 #define FK_CLASS_L2 69

@@ -423,7 +423,7 @@ def test_fast_and_generic_kernels_agree_bit_for_bit():
         outs = {}
         try:
             # 1 = generic kernel, 2 = fast kernels without TMA, 3 = row-partitioned fast kernel,
-            # 4 = fk_blur_cols for every class, 5 = fk_blur_bytes for every class (include/fovea.h)
+            # 4 = fk_blur_cols for every class, 5 = fk_blur_tma for every class (include/fovea.h)
             for variant in (1, 2, 3, 4, 5):
                 eng.set_kernel_variant(variant)
                 outs[variant] = fk.foveate_batch(frames, fix, p).clone()
@@ -436,7 +436,7 @@ def test_fast_and_generic_kernels_agree_bit_for_bit():
 
 def test_column_kernel_every_class_panels_and_strips_vs_generic():
     """1080p frames with fixations in a corner, on an edge and in the middle: every tap-count
-    class of fk_blur_cols and fk_blur_bytes is populated -- filters past 89 taps are walked in
+    class of fk_blur_cols and fk_blur_tma is populated -- filters past 89 taps are walked in
     tap panels by fk_blur_cols,
     same-filter fragments are merged into strips up to 128 rows, tiles hang over all four
     image borders -- and the result must equal the generic kernel's bit for bit (uint8 with

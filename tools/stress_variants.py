@@ -1,5 +1,5 @@
 """Repeatability / agreement stress: many 1080p frames with random fixations through the default
-dispatch (fk_blur_bytes, class launches side by side), fk_blur_cols everywhere (variant 4), the
+dispatch (fk_blur_tma, class launches side by side), fk_blur_cols everywhere (variant 4), the
 generic kernel (variant 1, first round) and the default kernels launched one class after the
 other (variant 16); all runs must be bit-identical.  usage: python tools/stress_variants.py [frames] [rounds]"""
 import sys
