@@ -35,16 +35,21 @@ int fk_cuda_fail(fk_handle *h, cudaError_t e, const char *what)
 
 static inline cudaStream_t as_stream(void *s) { return (cudaStream_t)s; }
 
-int fk_strip_rows_for(int n_frames)
+int fk_strip_rows_for(int n_frames, int width, int height)
 {
     static const int forced = [] {
         const char *e = getenv("FK_STRIP_ROWS_FORCE");
         return e ? atoi(e) : 0;
     }();
     if (forced > 0) return forced < FK_STRIP_ROWS ? forced : FK_STRIP_ROWS;
-    /* measured on 1080p / 32-pixel fragments: one frame streams fastest with 64-row strips
-     * (2 469 frames/s closed loop against 2 021 with 512), a 256-frame batch with the tallest */
-    return n_frames >= 8 ? FK_STRIP_ROWS : n_frames >= 4 ? 256 : n_frames >= 2 ? 128 : 64;
+    /* By the 32 x 32 pixel units of the batch (what the persistent CTAs have to share; 2 040 per
+     * 1080p frame), measured with the tall strips drawn first: one 1080p frame streams fastest
+     * with 64-row strips, 8-16 frames with 256 (0.54 of the roofline against 0.51 with 1 024 at
+     * 8 frames), 32 with 512, 64 and more with the tallest. */
+    const long long cells = (long long)n_frames * ((width + FK_RECT - 1) / FK_RECT) *
+                            ((height + FK_RECT - 1) / FK_RECT);
+    return cells >= 131072 ? FK_STRIP_ROWS : cells >= 65536 ? 512 : cells >= 8192 ? 256
+         : cells >= 4096 ? 128 : 64;
 }
 
 /* Host evaluation of the sigma chain (retinal.py:112-155) at distance d, used only to
@@ -384,7 +389,7 @@ int fk_plan_model(fk_plan *p, const fk_params *prm, int n_frames, const double *
     if (!p->d.self_zero)
         FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev no_density = {nullptr, 0, 0, 0.0};
-    p->d.strip_rows = fk_strip_rows_for(n_frames);
+    p->d.strip_rows = fk_strip_rows_for(n_frames, p->d.width, p->d.height);
     p->d.mixed = h->no_mixed ? 0 : 1;
     FK_CUDA(h, fk_launch_plan(p->d, *prm, n_frames, fix_dev, no_density, s));
     h->launches++;
@@ -450,7 +455,7 @@ int fk_plan_density(fk_plan *p, const fk_params *prm, int n_frames, const double
     p->custom = 0;
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
     const fk_density_dev den = {p->density_map, map_w, map_h, sigma_max};
-    p->d.strip_rows = fk_strip_rows_for(n_frames);
+    p->d.strip_rows = fk_strip_rows_for(n_frames, p->d.width, p->d.height);
     p->d.mixed = h->no_mixed ? 0 : 1;
     p->d.canonical = 1;
     p->d.self_zero = 0;
@@ -514,7 +519,7 @@ int fk_plan_set_grid(fk_plan *p, int shift_x, int shift_y, int grid_w, int grid_
     p->d.taps = p->custom_taps;
     p->custom = 1;
     FK_CUDA(h, cudaMemsetAsync(p->d.counters, 0, FK_COUNTER_WORDS * sizeof(int32_t), s));
-    p->d.strip_rows = fk_strip_rows_for(1);
+    p->d.strip_rows = fk_strip_rows_for(1, p->d.width, p->d.height);
     p->d.mixed = 0; /* a caller's bank: tap offsets are not the canonical r * r */
     p->d.canonical = 0;
     p->d.self_zero = 0;

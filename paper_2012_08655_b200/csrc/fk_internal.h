@@ -215,11 +215,11 @@ struct fk_plan {
     fk_plan_dev d{};
 };
 
-/* Tallest merged strip for a batch of n_frames: taller strips share more of the horizontal
- * pass (the 2r halo rows between merged fragments) and cost fewer item set-ups, shorter ones
- * give the persistent CTAs of a small batch enough items to share.  FK_STRIP_ROWS_FORCE in
- * the environment overrides it (tuning runs). */
-int fk_strip_rows_for(int n_frames);
+/* Tallest merged strip for a batch of n_frames frames of width x height pixels: taller strips
+ * share more of the horizontal pass (the 2r halo rows between merged fragments) and cost fewer
+ * item set-ups, shorter ones give the persistent CTAs of a small batch enough items to share.
+ * FK_STRIP_ROWS_FORCE in the environment overrides it (tuning runs). */
+int fk_strip_rows_for(int n_frames, int width, int height);
 
 /* error plumbing (fk_api.cu) */
 int fk_fail(fk_handle *h, int code, const char *fmt, ...);
