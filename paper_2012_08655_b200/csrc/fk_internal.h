@@ -45,8 +45,10 @@ enum {
  * walked in panels in class 4.  Class 5 (longer filters) goes to the generic kernel, class 6
  * holds the identity fragments (L = 1), plain copies.  (Merging classes 0-2 was measured:
  * nothing on uint8, 3-22 % slower on float32.) */
+#ifndef FK_CLASS_L0 /* -DFK_CLASS_L0=.. -DFK_CLASS_L1=..: class-boundary experiments */
 #define FK_CLASS_L0 23
 #define FK_CLASS_L1 47
+#endif
 #define FK_CLASS_L2 69
 #define FK_CLASS_L3 89
 #define FK_CLASS_L4 127
