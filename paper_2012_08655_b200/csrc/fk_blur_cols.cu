@@ -1498,7 +1498,7 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
     /* the intermediate: 2r rows the V pass still needs + the 32 of the next block.  A warp of
      * a mixed item whose filter is shorter than the item's longest is not aligned to the groups
      * of 8 output rows (up to 7 more rows wait for their group), hence 8 rows of slack */
-    const bool mixed_items = pd.mixed && pd.fragment < FK_RECT && (pd.fragment & 7) == 0; /* fk_emit_items */
+    const bool mixed_items = pd.mixed && pd.fragment < FK_RECT && (pd.fragment & 7) == 0; /* holds_mixed_items */
     const int icap = (2 * r + kTB + (mixed_items ? 8 : 0) + 3) & ~3;
     const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
     size_t smem = (size_t)nq * kQStride + 128 +
@@ -1545,6 +1545,13 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
 
 } // namespace
 
+/* Only fk_blur_tma reads mixed items (fk_internal.h); a plan holds them when it was emitted
+ * with pd.mixed for fragments of 8 or 16 pixels (fk_emit_items). */
+static bool holds_mixed_items(const fk_plan_dev &pd)
+{
+    return pd.mixed && pd.fragment < FK_RECT && (pd.fragment & 7) == 0;
+}
+
 bool fk_blur_tma_usable(const void *in, int width, int height, int is_f32)
 {
     (void)height;
@@ -1569,6 +1576,7 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
             cudaError_t e = launch_tma<float>(h, pd, klass, in, out, n_frames, class_length, s, taken);
             if (e != cudaSuccess || *taken) return e;
         }
+        if (holds_mixed_items(pd)) return cudaErrorNotSupported; /* fk_render_any re-emits first */
         return launch_cols<float, false>(h, map, pd, klass, in, out, class_length, s, taken);
     }
     /* uint8 by TMA: fk_blur_tma, the kernel whose H pass reads the TMA bytes directly -- no
@@ -1578,6 +1586,7 @@ cudaError_t fk_launch_blur_cols(fk_handle *h, const fk_plan_dev &pd, int klass, 
         cudaError_t e = launch_tma<uint8_t>(h, pd, klass, in, out, n_frames, class_length, s, taken);
         if (e != cudaSuccess || *taken) return e;
     }
+    if (holds_mixed_items(pd)) return cudaErrorNotSupported; /* fk_render_any re-emits first */
     const bool tma = h->variant != 2 && make_tensor_map(&map, in, pd.width, pd.height, kC, n_frames);
     if (tma) return launch_cols<uint8_t, true>(h, map, pd, klass, in, out, class_length, s, taken);
     return launch_cols<uint8_t, false>(h, map, pd, klass, in, out, class_length, s, taken);
