@@ -50,6 +50,8 @@
  * v_task_px), at the end for h_part; every shared-memory word a padded tap can touch holds a
  * finite value so 0 * garbage never produces a NaN.
  */
+#include <cstdlib>
+
 #include "fk_stage.cuh"
 
 /*
@@ -791,23 +793,40 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
  * fk_blur_tma -- RGB frames staged by TMA: the H pass reads what landed directly (uint8 below;
  * float32: h_float).
  *
- * No working tile, no conversion pass, no CTA barrier.  One 4-D TMA box per 32-row block,
- * over the batch seen as (16 bytes, rows, 16-byte chunks of a row, frames), lands the block
- * as raw[chunk][row][16 B]: consecutive rows are 16 bytes apart, so lane = row reads are
- * spread over all banks.  A lane walks its row as a stream of aligned 32-bit words: per
- * chunk of four taps three new words, a funnel shift each to undo the byte misalignment of
- * the tile, and one PRMT per byte into the denormal-linear fp32 encoding (bytes_to_float4_s)
- * -- all on the integer pipe, under the 96 FFMAs of the chunk.  The word addresses repeat
- * every 12 words (three chunks of 16 bytes) up to a constant, so a lane keeps 12 address
- * registers and bumps each after use.  Rows clamp in y by picking the box row; columns
- * outside the image are patched in the raw bytes (edge items only, with a CTA barrier).
+ * No working tile, no conversion pass, no CTA barrier.  The batch is seen as a 4-D tensor
+ * (16 bytes, 16-byte units of a row, rows, frames) and a block of tile rows lands as
+ * raw[row][nq units of 16 B]: the kernel gets
+ * a family of tensor maps whose boxes are 32 rows of nq units for a few odd nq, and an item
+ * picks the narrowest that holds its filter (one box shape per class launch, wide enough for
+ * the class's longest filter, moves 20-30 % more bytes from the L2 on float32 frames, whose
+ * blocks are four times the size; boxes of fewer rows for the short first and last blocks of
+ * an item were measured as well: nothing).  The row pitch 16 nq with nq odd
+ * spreads lane = row reads of 128 bits over all banks.  uint8: a lane walks its row as a stream
+ * of aligned 32-bit words from one address register (immediate offsets over a turn of four
+ * chunks): per chunk of four taps three new words, a funnel shift each to undo the byte
+ * misalignment of the tile, and one PRMT per byte into the denormal-linear fp32 encoding
+ * (bytes_to_float4_s) -- all on the integer pipe, under the 96 FFMAs of the chunk.  Rows clamp
+ * in y by picking the box row; columns outside the image are patched in the raw bytes (edge
+ * items only, with a CTA barrier).
  * Everything after the H pass (transposed intermediate, V pass, dealing of items, taps) is
  * fk_blur_cols.  Synchronisation: per raw buffer (one or two) a `bar` (TMA bytes landed, all
  * warps wait) and an `hbar` ("H pass done", one arrival per warp; thread 0 waits for it before
  * it requests the block that goes into that buffer next).
  * ===================================================================================== */
-constexpr int kQB = 16;            /* bytes per chunk */
-constexpr int kQStride = kQB * kTB; /* bytes between chunks in shared memory: 512 */
+constexpr int kQB = 16;      /* bytes per unit of a row: a chunk of 16 bytes / a quad of floats */
+constexpr int kMapWidths = 6; /* box widths per launch */
+/* 16-byte units of a row that a lane's stream reads for a filter of `length` taps.  uint8: 15
+ * bytes of skew + 96 + 12 per chunk of taps + what the window loads ahead; float32: the last
+ * warp starts at quad 18 and reads 9 + 3 per chunk of taps but the last (what the last chunk
+ * loads ahead is never used and may come from whatever follows the block in shared memory). */
+template <typename T> __host__ __device__ __forceinline__ int tma_units_for(int length)
+{
+    return sizeof(T) == 1 ? (168 + 6 * ((length - 1) >> 1) + kQB - 1) / kQB
+                          : 18 + 6 + 3 * ((length + 6) >> 2);
+}
+struct fk_tmaps {
+    CUtensorMap m[kMapWidths]; /* boxes of kTB rows x (nq - (j << nq_shift)) units */
+};
 
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar,
                                             int c0, int c1, int c2, int c3)
@@ -827,27 +846,17 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr)
 
 /*
  * Horizontal task on raw bytes: acc[j] += sum_k g[k] * byte[b0 + j + 3k], j in [0, 24), for one
- * row.  `row_s` is the shared address of the row inside chunk 0 of the block, b0 the byte of
- * the row (from the start of chunk 0) that is input 0 of this task.
+ * row.  `row_s` is the shared address of the row's first byte in the raw block, b0 the byte
+ * of the row that is input 0 of this task.
  */
 __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, int nchunk, int zpad,
                                         float (&acc)[kSegF])
 {
     constexpr int C = kC, NW = 16 * C;
     float win[NW];
-    uint32_t ad[12]; /* addresses of the next 12 words of the stream */
-    const int w0 = b0 >> 2;
+    /* word i of the stream lies at a + 4 i; `a` advances by 12 words per turn of four chunks */
+    uint32_t a = row_s + (uint32_t)((b0 >> 2) * 4);
     const uint32_t bsh = (uint32_t)(b0 & 3) * 8u;
-#pragma unroll
-    for (int i = 0; i < 12; i++) {
-        const int w = w0 + i;
-        ad[i] = row_s + (uint32_t)((w >> 2) * kQStride + (w & 3) * 4);
-    }
-    auto next_word = [&](const int i) { /* word i (mod 12) of the stream, then step its address */
-        const uint32_t v = lds32(ad[i]);
-        ad[i] += 3 * kQStride;
-        return v;
-    };
     auto put = [&](const int slot4, uint32_t lo, uint32_t hi) { /* four floats from one shifted word */
         const float4 f = bytes_to_float4_s(__funnelshift_r(lo, hi, bsh));
         win[slot4 + 0] = f.x;
@@ -856,28 +865,30 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
         win[slot4 + 3] = f.w;
     };
     /* words 0..9: inputs 0..35 (slots 0..2); word 9 is carried as the low half of the next */
-    uint32_t carry = next_word(0);
+    uint32_t carry = lds32(a);
 #pragma unroll
     for (int k = 0; k < 9; k++) {
-        const uint32_t nx = next_word(k + 1);
+        const uint32_t nx = lds32(a + 4u * (uint32_t)(k + 1));
         put(4 * k, carry, nx);
         carry = nx;
     }
-    /* words 10, 11, 0 (of the next turn): loaded a chunk ahead of their conversion */
-    uint32_t n0 = next_word(10), n1 = next_word(11), n2 = next_word(0);
+    /* words 10, 11, 12: loaded a chunk ahead of their conversion */
+    uint32_t n0 = lds32(a + 40), n1 = lds32(a + 44), n2 = lds32(a + 48);
     float4 g4 = lds128(wts);
     uint32_t wa = wts + 16;
     /* slot p+3 <- the three words loaded during the previous chunk, then load the next three:
-     * stream indices 13 + 3c .. 15 + 3c = (1 + 3p) .. (3 + 3p) mod 12 */
+     * words 13 + 3c .. 15 + 3c of the stream for chunk c, i.e. 1 + 3p' .. 3 + 3p' past the
+     * turn's first word with p' = p, or 4 for p = 0 (the last chunk of a turn) */
     auto refill = [&](const int p) {
         const int q = ((p + 3) % 4) * 4 * C;
         put(q + 0, carry, n0);
         put(q + 4, n0, n1);
         put(q + 8, n1, n2);
         carry = n2;
-        n0 = next_word((1 + 3 * p) % 12);
-        n1 = next_word((2 + 3 * p) % 12);
-        n2 = next_word((3 + 3 * p) % 12);
+        const uint32_t o = 4u * (uint32_t)(1 + 3 * (p == 0 ? 4 : p));
+        n0 = lds32(a + o);
+        n1 = lds32(a + o + 4);
+        n2 = lds32(a + o + 8);
     };
     auto chunk = [&](const int p) {
         const float g[4] = {g4.x, g4.y, g4.z, g4.w};
@@ -912,6 +923,7 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
             }
         }
     }
+    a += 48; /* the first chunk closed turn 0 */
     for (int c = 1; c < nchunk; c += 4) {
         chunk(1);
         if (c + 1 >= nchunk) break;
@@ -920,6 +932,7 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
         chunk(3);
         if (c + 3 >= nchunk) break;
         chunk(0);
+        a += 48;
     }
 }
 
@@ -929,14 +942,14 @@ __device__ __forceinline__ void h_bytes(uint32_t row_s, int b0, uint32_t wts, in
  * float is 3 (x0 - r).  The residue is absorbed by the TAPS: the stream starts zf = (x0 - r)
  * mod 4 pixels left of the tile, on a pixel that is a multiple of four (a float that is a
  * multiple of 12, quad-aligned), and the filter is padded with zf zeros in front and zb at
- * the end up to a multiple of four taps.  The block lands as raw[quad][row][4 floats] with
- * stream float 0 at raw float 0, so a lane's stream is one LDS.128 per quad, kQStride bytes
- * apart: no shift, no conversion.  Zero taps are never multiplied -- the image may hold
+ * the end up to a multiple of four taps.  The block lands as raw[row][quads] with stream
+ * float 0 at raw float 0, so a lane's stream is one LDS.128 per quad: no shift, no conversion
+ * (the row pitch is an odd number of quads: conflict-free).  Zero taps are never multiplied -- the image may hold
  * anything beyond the filter's support, and a partial first / last chunk costs what its
  * real taps cost: the first and the last chunk of a task run a copy of the chunk whose four
  * tap groups are guarded (uniform branches), the chunks in between the plain one.
- * `row_s` is the shared address of the lane's row inside the first quad of the warp's
- * columns, `wts` of the padded taps, nchunk = (zf + L + zb) / 4.
+ * `row_s` is the shared address of the first quad of the warp's columns in the lane's row,
+ * `wts` of the padded taps, nchunk = (zf + L + zb) / 4.
  */
 __device__ __forceinline__ void h_float(uint32_t row_s, uint32_t wts, int nchunk, int zf, int zb,
                                         float (&acc)[kSegF])
@@ -945,7 +958,7 @@ __device__ __forceinline__ void h_float(uint32_t row_s, uint32_t wts, int nchunk
     float win[NW];
 #pragma unroll
     for (int v = 0; v < 3 * C; v++) {
-        const float4 x = lds128(row_s + (uint32_t)(v * kQStride));
+        const float4 x = lds128(row_s + (uint32_t)(v * kQB));
         win[4 * v + 0] = x.x;
         win[4 * v + 1] = x.y;
         win[4 * v + 2] = x.z;
@@ -953,20 +966,20 @@ __device__ __forceinline__ void h_float(uint32_t row_s, uint32_t wts, int nchunk
     }
 #pragma unroll
     for (int j = 0; j < kSegF; j++) acc[j] = 0.0f;
-    uint32_t nxt = row_s + 3 * C * kQStride;
+    uint32_t nxt = row_s + 3 * C * kQB;
     float4 g4 = lds128(wts);
     uint32_t wa = wts + 16;
     auto refill = [&](const int p) { /* ring slot p + 3 <- the next three quads of the row */
 #pragma unroll
         for (int v = 0; v < C; v++) {
-            const float4 x = lds128(nxt + (uint32_t)(v * kQStride));
+            const float4 x = lds128(nxt + (uint32_t)(v * kQB));
             const int q = (((p + 3) % 4) * C + v) * 4;
             win[q + 0] = x.x;
             win[q + 1] = x.y;
             win[q + 2] = x.z;
             win[q + 3] = x.w;
         }
-        nxt += C * kQStride;
+        nxt += C * kQB;
     };
     auto chunk = [&](const int p) {
         const float g[4] = {g4.x, g4.y, g4.z, g4.w};
@@ -1021,14 +1034,15 @@ __device__ __forceinline__ void h_float(uint32_t row_s, uint32_t wts, int nchunk
  * here.  Four threads per box row; `e0` is the image float of stream float 0 (a multiple of
  * 3, so the channel of stream float j is j mod 3), `n` the stream floats that meet taps.
  */
-__device__ __noinline__ void patch_x_edges_f32(unsigned char *raw, const float *__restrict__ src,
-                                               int e0, int n, int WC, int ys_c, int H, int tid)
+__device__ __noinline__ void patch_x_edges_f32(unsigned char *raw, int pitch,
+                                               const float *__restrict__ src, int e0, int n, int WC,
+                                               int ys_c, int H, int tid)
 {
     const int row = tid >> 2;
     const int gy = ys_c + row < H - 1 ? ys_c + row : H - 1;
     const float *grow = src + (size_t)gy * WC;
-    float *rrow = reinterpret_cast<float *>(raw + row * kQB);
-    auto put = [&](int j, int gi) { rrow[(j >> 2) * (kQStride / 4) + (j & 3)] = __ldg(grow + gi); };
+    float *rrow = reinterpret_cast<float *>(raw + row * pitch);
+    auto put = [&](int j, int gi) { rrow[j] = __ldg(grow + gi); };
     const int nl = e0 < 0 ? (-e0 < n ? -e0 : n) : 0;
 #pragma unroll 1
     for (int j = tid & 3; j < nl; j += 4) put(j, j % kC);
@@ -1076,17 +1090,19 @@ template <typename T, bool MIXED> __device__ __forceinline__ int box_unit(const 
  * geometry below folds into the item's at compile time. */
 template <typename T, int MINB, bool MIXED>
 __global__ void __launch_bounds__(kThreads, MINB)
-fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *__restrict__ in,
-            T *__restrict__ out, int klass, int wts_floats, int nq, int icap, int ipitch, int nbuf)
+fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__restrict__ in,
+            T *__restrict__ out, int klass, int wts_floats, int nq, int nq_shift, int icap, int ipitch,
+            int nbuf)
 {
     constexpr int C = kC;
     constexpr bool kBytes = sizeof(T) == 1;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    /* layout: [raw x nbuf: nq chunks x 32 rows x 16 B][barriers + item slots, 128 B][per-warp taps x 3][ring]
-     * nbuf = 2 where a second raw buffer does not cost a resident CTA: the TMA request then
+    /* layout: [raw x nbuf: 32 rows x nq units of 16 B at most][barriers + item slots, 128 B][per-warp taps x 3][ring]
+     * nq: units per row of the widest box (the class's longest filter), 1 << nq_shift: units
+     * between box widths.  nbuf = 2 where a second raw buffer does not cost a resident CTA: the TMA request then
      * runs two blocks ahead of the H pass instead of one, so the first blocks of an item --
      * which have no V pass yet to hide the fetch under -- do not wait for their bytes. */
-    const int raw_bytes = nq * kQStride;
+    const int raw_bytes = nq * kQB * kTB;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + nbuf * raw_bytes); /* [2] bytes landed */
     uint64_t *hbar = bar + 2;                                                   /* [2] H pass done */
     int *slot_idx = reinterpret_cast<int *>(bar + 4);                 /* [2] */
@@ -1106,13 +1122,21 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
     auto load_item = [&](int i) {
         return i < n_items ? __ldg(reinterpret_cast<const uint4 *>(list.at(i))) : none;
     };
-    /* One 32-row block: the box starts at the 16-byte chunk that holds the tile's first byte
+    /* Box width of an item: index into the launch's widths (0 = widest) of the narrowest one
+     * that holds the units a lane's stream reads (tma_units_for, evaluated by launch_tma for the
+     * class's longest filter). */
+    auto width_of = [&](const item_geo &g) {
+        const int j = (nq - tma_units_for<T>(g.L)) >> nq_shift;
+        return j < kMapWidths - 1 ? j : kMapWidths - 1;
+    };
+    /* One 32-row block: the box starts at the 16-byte unit that holds the stream's first byte
      * (possibly left of the image: TMA fills what is outside with zeros) and at the first
      * source row clamped into the image. */
     auto issue = [&](const item_geo &g, int rb, int buf) {
         const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
-        mbar_expect_tx(bar + buf, (uint32_t)raw_bytes);
-        tma_load_4d(smem_raw + buf * raw_bytes, &tmap, bar + buf, 0, ys_c, box_unit<T, MIXED>(g), g.f);
+        const int j = width_of(g);
+        mbar_expect_tx(bar + buf, (uint32_t)((nq - (j << nq_shift)) * kQB * kTB));
+        tma_load_4d(smem_raw + buf * raw_bytes, &tmaps.m[j], bar + buf, 0, box_unit<T, MIXED>(g), ys_c, g.f);
     };
     auto fill_taps = [&](const uint4 q, int slot) {
         const int L = MIXED ? warp_length(q, warp) : (int)((q.z >> 8) & 0x1fffu);
@@ -1217,6 +1241,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
         }
         T *dst = out + (size_t)g.f * H * W * C;
         const int box0 = box_unit<T, MIXED>(g) * (kBytes ? 16 : 4); /* image element of the box's first */
+        const int pitch = (nq - (width_of(g) << nq_shift)) * kQB;   /* bytes between rows of the raw block */
         /* the warp's stream (element 0 meets the first tap, padding included) inside the box */
         const int sw = (xw - zf) * C - box0;
         const int skew = (x0 - r) * C - box0;                      /* tile float 0 = raw element skew */
@@ -1251,7 +1276,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
             }
             if (!kBytes) {
                 if (box0 < 0 || skew + tw > W * C - box0) {
-                    patch_x_edges_f32(raw, reinterpret_cast<const float *>(in) + (size_t)g.f * H * W * C,
+                    patch_x_edges_f32(raw, pitch, reinterpret_cast<const float *>(in) + (size_t)g.f * H * W * C,
                                       box0, skew + tw, W * C, ys_c, H, tid);
                     __syncthreads();
                 }
@@ -1263,8 +1288,8 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
                  * with what is there (only the chunk at the image border keeps any of it --
                  * whatever lies beyond the tile's ends meets zero taps only). */
                 const int prow = warp * kWR + (lane >> 2);
-                unsigned char *rowp = raw + prow * kQB;
-                auto at = [&](int m) -> uint32_t { return rowp[(m >> 4) * kQStride + (m & 15)]; };
+                unsigned char *rowp = raw + prow * pitch;
+                auto at = [&](int m) -> uint32_t { return rowp[m]; };
                 auto lowbytes = [](int n) { return n >= 4 ? 0xffffffffu : n <= 0 ? 0u : (1u << (8 * n)) - 1u; };
                 auto fill = [&](int e, int A, int B) { /* bytes [A, B) <- pixel at byte e */
                     const uint32_t px = at(e) | (at(e + 1) << 8) | (at(e + 2) << 16);
@@ -1275,7 +1300,7 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
                         const int m0 = q * 16;
                         int ph = (m0 - e) % 3; /* channel of the chunk's first byte */
                         ph = ph < 0 ? ph + 3 : ph;
-                        uint4 *cp = reinterpret_cast<uint4 *>(rowp + q * kQStride);
+                        uint4 *cp = reinterpret_cast<uint4 *>(rowp + q * kQB);
                         uint4 v = *cp;
                         uint32_t *w = &v.x;
 #pragma unroll
@@ -1303,9 +1328,9 @@ fk_blur_tma(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd, const T *_
                 float hacc[kSegF];
                 const int brow = fast_clamp(ys + lane, 0, H - 1) - ys_c; /* box row */
                 if (kBytes)
-                    h_bytes(raw_s + (uint32_t)(brow * kQB), sw, smem_u32(w_h), nchunk, zpad, hacc);
+                    h_bytes(raw_s + (uint32_t)(brow * pitch), sw, smem_u32(w_h), nchunk, zpad, hacc);
                 else
-                    h_float(raw_s + (uint32_t)(brow * kQB + (sw >> 2) * kQStride), smem_u32(w_h),
+                    h_float(raw_s + (uint32_t)(brow * pitch + (sw >> 2) * kQB), smem_u32(w_h),
                             nchunk_h, zf, 4 * nchunk_h - zf - Lw, hacc);
                 int rr = rbm + lane + zpad; /* zpad rows down: see v_task_px */
                 rr = rr >= icap ? rr - icap : rr;
@@ -1445,38 +1470,26 @@ cudaError_t launch_cols(fk_handle *h, const CUtensorMap &map, const fk_plan_dev 
     return cudaGetLastError();
 }
 
-/* uint8: the batch as (16 bytes, rows, 16-byte chunks of a row, frames) with boxes of
- * 16 B x 32 rows x nq chunks: lands as [chunk][row][16 B] in shared memory. */
-bool make_tensor_map_chunks(CUtensorMap *map, const void *in, int W, int H, int n_frames, int nq)
+/* The batch as a 4-D tensor (16 bytes, 16-byte units of a row, rows, frames) -- uint8: 16-byte
+ * chunks, float32: quads of floats -- with boxes of 16 B x nq units x `rows` rows, which land as
+ * [row][nq units] in shared memory. */
+template <typename T>
+bool make_tensor_map_rows(CUtensorMap *map, const void *in, int W, int H, int n_frames, int nq, int rows)
 {
     encode_tiled_fn enc = get_encode_tiled();
-    const size_t pitch = (size_t)W * kC;
-    if (!enc || ((uintptr_t)in & 15) != 0 || (pitch & 15) != 0 || nq > 256) return false;
-    cuuint64_t dims[4] = {(cuuint64_t)kQB, (cuuint64_t)H, (cuuint64_t)(pitch / kQB), (cuuint64_t)n_frames};
-    cuuint64_t strides[3] = {(cuuint64_t)pitch, (cuuint64_t)kQB, (cuuint64_t)pitch * H};
-    cuuint32_t box[4] = {(cuuint32_t)kQB, (cuuint32_t)kTB, (cuuint32_t)nq, 1};
+    constexpr int per_unit = kQB / (int)sizeof(T); /* elements per unit */
+    const size_t row_elems = (size_t)W * kC;
+    if (!enc || ((uintptr_t)in & 15) != 0 || (row_elems % per_unit) != 0 || nq > 256) return false;
+    const size_t pitch = row_elems * sizeof(T);
+    cuuint64_t dims[4] = {(cuuint64_t)per_unit, (cuuint64_t)(row_elems / per_unit), (cuuint64_t)H,
+                          (cuuint64_t)n_frames};
+    cuuint64_t strides[3] = {(cuuint64_t)kQB, (cuuint64_t)pitch, (cuuint64_t)pitch * H};
+    cuuint32_t box[4] = {(cuuint32_t)per_unit, (cuuint32_t)nq, (cuuint32_t)rows, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(in), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-/* float32: the batch as (4 floats, rows, quads of a row, frames) with boxes of
- * 4 floats x 32 rows x nq quads: lands as [quad][row][4 floats] in shared memory. */
-bool make_tensor_map_quads(CUtensorMap *map, const void *in, int W, int H, int n_frames, int nq)
-{
-    encode_tiled_fn enc = get_encode_tiled();
-    const size_t rowf = (size_t)W * kC;
-    if (!enc || ((uintptr_t)in & 15) != 0 || (rowf & 3) != 0 || nq > 256) return false;
-    const size_t pitch = rowf * sizeof(float);
-    cuuint64_t dims[4] = {4, (cuuint64_t)H, (cuuint64_t)(rowf / 4), (cuuint64_t)n_frames};
-    cuuint64_t strides[3] = {(cuuint64_t)pitch, (cuuint64_t)kQB, (cuuint64_t)pitch * H};
-    cuuint32_t box[4] = {4, (cuuint32_t)kTB, (cuuint32_t)nq, 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void *>(in), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     4, const_cast<void *>(in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -1491,24 +1504,29 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
     /* float32: up to three more zeros in front of the H pass's taps (h_float) */
     const int nchunk_h = bytes ? nchunk : (class_length + 6) / 4;
     const int wts_floats = 4 * nchunk_h + 4;
-    /* chunks / quads a lane's stream can reach: uint8 -- 15 bytes of skew + 96 + 12 per chunk
-     * of taps + what the window loads ahead; float32 -- the last warp starts at quad 18 and
-     * reads 9 + 3 per chunk of taps */
-    const int nq = bytes ? (168 + 6 * r + kQB - 1) / kQB : 18 + 9 + 3 * nchunk_h;
+    /* Box widths: the widest holds the class's longest filter, the narrowest its shortest; odd
+     * numbers of units, so that the rows of a block -- 16 nq bytes apart -- spread over all
+     * banks when every lane reads 128 bits of its own row. */
+    const int nq = tma_units_for<T>(class_length) | 1;
+    const int nq_lo = tma_units_for<T>(fk_class_lmin(klass) < class_length ? fk_class_lmin(klass) : class_length);
+    int nq_shift = 1; /* widths 2, 4 or 8 units apart: the narrowest box about the class's shortest filter */
+    while (nq_shift < 3 && nq - ((kMapWidths - 1) << nq_shift) > nq_lo) nq_shift++;
     /* the intermediate: 2r rows the V pass still needs + the 32 of the next block.  A warp of
      * a mixed item whose filter is shorter than the item's longest is not aligned to the groups
      * of 8 output rows (up to 7 more rows wait for their group), hence 8 rows of slack */
     const bool mixed_items = pd.mixed && pd.fragment < FK_RECT && (pd.fragment & 7) == 0; /* holds_mixed_items */
     const int icap = (2 * r + kTB + (mixed_items ? 8 : 0) + 3) & ~3;
     const int ipitch = (icap & 7) == 4 ? icap : icap + 4;
-    size_t smem = (size_t)nq * kQStride + 128 +
+    const size_t raw_bytes = (size_t)nq * kQB * kTB;
+    size_t smem = raw_bytes + 128 +
                   ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
     if (smem > h->prop.sharedMemPerBlockOptin) return cudaSuccess;
-    CUtensorMap map;
-    memset(&map, 0, sizeof map);
-    if (bytes ? !make_tensor_map_chunks(&map, in, pd.width, pd.height, n_frames, nq)
-              : !make_tensor_map_quads(&map, in, pd.width, pd.height, n_frames, nq))
-        return cudaSuccess;
+    fk_tmaps maps;
+    memset(&maps, 0, sizeof maps);
+    for (int j = 0; j < kMapWidths; j++) {
+        const int w = nq - (j << nq_shift) > 1 ? nq - (j << nq_shift) : 1; /* never picked below nq_lo */
+        if (!make_tensor_map_rows<T>(&maps.m[j], in, pd.width, pd.height, n_frames, w, kTB)) return cudaSuccess;
+    }
     /* Layouts that fit three times on an SM run with the register budget of three resident
      * CTAs, the others with that of two. */
     const size_t per_sm = h->prop.sharedMemPerMultiprocessor;
@@ -1524,21 +1542,23 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
     if (occ < 1) return cudaSuccess;
     /* a second raw buffer where it does not cost a resident CTA (variant 6: never) */
     int nbuf = 1;
-    const size_t smem2 = smem + (size_t)nq * kQStride;
+    const size_t smem2 = smem + raw_bytes;
     if (smem2 <= h->prop.sharedMemPerBlockOptin && h->variant != 6) {
         e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         if (e != cudaSuccess) return e;
         int occ2 = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, kernel, kThreads, smem2);
         if (e != cudaSuccess) return e;
-        if (occ2 >= occ) {
+        static const int force2 = getenv("FK_NBUF_FORCE") ? atoi(getenv("FK_NBUF_FORCE")) : 0;
+        if (occ2 >= occ || (force2 && occ2 >= 1 && occ2 + force2 >= occ)) {
             nbuf = 2;
             smem = smem2;
+            occ = occ2 < occ ? occ2 : occ;
         }
     }
     const int grid = h->prop.multiProcessorCount * occ;
-    kernel<<<grid, kThreads, smem, s>>>(map, pd, (const T *)in, (T *)out, klass, wts_floats, nq,
-                                        icap, ipitch, nbuf);
+    kernel<<<grid, kThreads, smem, s>>>(maps, pd, (const T *)in, (T *)out, klass, wts_floats, nq,
+                                        nq_shift, icap, ipitch, nbuf);
     *taken = true;
     return cudaGetLastError();
 }
