@@ -1522,10 +1522,24 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
                   ((size_t)kWarps * 3 * wts_floats + (size_t)kRowF * ipitch) * sizeof(float);
     if (smem > h->prop.sharedMemPerBlockOptin) return cudaSuccess;
     fk_tmaps maps;
-    memset(&maps, 0, sizeof maps);
-    for (int j = 0; j < kMapWidths; j++) {
-        const int w = nq - (j << nq_shift) > 1 ? nq - (j << nq_shift) : 1; /* never picked below nq_lo */
-        if (!make_tensor_map_rows<T>(&maps.m[j], in, pd.width, pd.height, n_frames, w, kTB)) return cudaSuccess;
+    static_assert(sizeof(fk_tmaps) == sizeof(fk_handle::tmap_slot::maps), "tensor-map cache slot");
+    fk_handle::tmap_slot &slot = h->tmap_cache[(bytes ? 0 : FK_NCLASS) + klass];
+    if (slot.in == in && slot.width == pd.width && slot.height == pd.height && slot.frames == n_frames &&
+        slot.nq == nq && slot.shift == nq_shift) {
+        memcpy(&maps, slot.maps, sizeof maps);
+    } else {
+        memset(&maps, 0, sizeof maps);
+        for (int j = 0; j < kMapWidths; j++) {
+            const int w = nq - (j << nq_shift) > 1 ? nq - (j << nq_shift) : 1; /* never picked below nq_lo */
+            if (!make_tensor_map_rows<T>(&maps.m[j], in, pd.width, pd.height, n_frames, w, kTB)) return cudaSuccess;
+        }
+        memcpy(slot.maps, &maps, sizeof maps);
+        slot.in = in;
+        slot.width = pd.width;
+        slot.height = pd.height;
+        slot.frames = n_frames;
+        slot.nq = nq;
+        slot.shift = nq_shift;
     }
     /* Layouts that fit three times on an SM run with the register budget of three resident
      * CTAs, the others with that of two. */

@@ -200,6 +200,14 @@ struct fk_handle {
     /* scratch for the FP32 peak probe */
     float *probe = nullptr;
     double *ssim_stats = nullptr; /* [3] device scratch of fk_ssim_stats */
+    /* the tensor maps of the last fk_blur_tma launch per (element type, class): a render of the
+     * same buffer with the same geometry (a stream of frames through one buffer, a bench loop)
+     * does not encode them again */
+    struct tmap_slot {
+        const void *in = nullptr;
+        int width = 0, height = 0, frames = 0, nq = 0, shift = 0;
+        alignas(64) unsigned char maps[6 * 128];
+    } tmap_cache[2 * FK_NCLASS];
 };
 
 struct fk_plan {

@@ -493,6 +493,29 @@ def test_tma_path_border_and_interior_tiles_vs_generic():
 
 
 @pytest.mark.gpu
+def test_tensor_maps_follow_the_buffer_geometry():
+    """fk_blur_tma keeps the tensor maps of its last launch per class (csrc/fk_internal.h,
+    tmap_cache): the same storage rendered as another geometry, as more or fewer frames, and
+    another buffer of the same geometry must each get maps of their own."""
+    eng = fk.get_engine(0)
+    rng = np.random.default_rng(77)
+    store = torch.from_numpy(rng.integers(0, 256, (4 * 128 * 256 * 3,), dtype=np.uint8)).cuda()
+    other = torch.from_numpy(rng.integers(0, 256, (4 * 128 * 256 * 3,), dtype=np.uint8)).cuda()
+    p = fk.FoveationParams(strength=1.5)
+    for buf, shape in ((store, (4, 128, 256, 3)), (store, (4, 256, 128, 3)), (store, (2, 256, 256, 3)),
+                       (other, (2, 256, 256, 3)), (store, (4, 128, 256, 3))):
+        n, h, w, _ = shape
+        frames = buf[: n * h * w * 3].view(shape)
+        fix = np.stack([np.linspace(0, w - 1, n), np.linspace(h - 1, 0, n)], axis=1)
+        try:
+            eng.set_kernel_variant(1)
+            ref = fk.foveate_batch(frames, fix, p).clone()
+        finally:
+            eng.set_kernel_variant(0)
+        assert torch.equal(fk.foveate_batch(frames, fix, p), ref), shape
+
+
+@pytest.mark.gpu
 def test_strip_height_does_not_change_the_output():
     """Merging same-filter fragments into strips is exact (an output pixel depends only on the
     image and its filter), whatever the cap on the strip height: the batch default (1 024 rows),
