@@ -1107,6 +1107,7 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     uint64_t *hbar = bar + 2;                                                   /* [2] H pass done */
     int *slot_idx = reinterpret_cast<int *>(bar + 4);                 /* [2] */
     uint4 *slot_desc = reinterpret_cast<uint4 *>(bar + 6);            /* [2], 16-byte aligned */
+    int4 *cur_rec = reinterpret_cast<int4 *>(bar + 12);               /* [2]: thread 0's request cursor */
     float *wts = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(bar) + 128);
     float *ring = wts + kWarps * 3 * wts_floats;
     const uint32_t ring_s = smem_u32(ring);
@@ -1128,15 +1129,6 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     auto width_of = [&](const item_geo &g) {
         const int j = (nq - tma_units_for<T>(g.L)) >> nq_shift;
         return j < kMapWidths - 1 ? j : kMapWidths - 1;
-    };
-    /* One 32-row block: the box starts at the 16-byte unit that holds the stream's first byte
-     * (possibly left of the image: TMA fills what is outside with zeros) and at the first
-     * source row clamped into the image. */
-    auto issue = [&](const item_geo &g, int rb, int buf) {
-        const int ys_c = fast_clamp(g.y0 - g.r + rb, 0, H - 1);
-        const int j = width_of(g);
-        mbar_expect_tx(bar + buf, (uint32_t)((nq - (j << nq_shift)) * kQB * kTB));
-        tma_load_4d(smem_raw + buf * raw_bytes, &tmaps.m[j], bar + buf, 0, box_unit<T, MIXED>(g), ys_c, g.f);
     };
     auto fill_taps = [&](const uint4 q, int slot) {
         const int L = MIXED ? warp_length(q, warp) : (int)((q.z >> 8) & 0x1fffu);
@@ -1171,32 +1163,49 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     if (idx < n_items) fill_taps(q_cur, 0);
     __syncthreads();
 
-    /* Thread 0's request cursor: the block to fetch next -- item `cq`, tile row `crb` -- runs
-     * nbuf blocks ahead of the H pass and `clead` items ahead of the item loop (every item has
-     * at least two blocks, so at most two: the next item, or the one drawn for after it). */
+    /* Thread 0's request cursor: the block to fetch next -- tile row `crb` of the item whose
+     * request record lies in shared memory -- runs nbuf blocks ahead of the H pass and `clead`
+     * items ahead of the item loop (every item has at least two blocks, so at most two: the next
+     * item, or the one drawn for after it).  The hand-over of a raw buffer is the one serial
+     * step of the CTA (warp 0 waits for the other warps' H passes, then thread 0 requests the
+     * next block while 31 lanes idle), so everything a request needs that does not change from
+     * block to block -- box unit and width, frame, first tile row, tile rows, rows of the first
+     * block -- is worked out once per item and kept as a 32-byte record that only thread 0
+     * writes and reads. */
     int d_idx = n_items;
     uint4 d_q = none;
-    uint4 cq = q_cur;
     bool cvalid = idx < n_items;
     int crb = 0, clead = 0, ibuf = 0;
-    auto request_next = [&]() {
-        if (!cvalid) return;
-        const item_geo g = decode_item<C>(cq, W);
+    auto cursor_to = [&](const uint4 q) {
+        const item_geo g = decode_item<C>(q, W);
         const int lead = (2 * g.r) & (kTB - 1);
         const int n_first = lead == 0 || lead > g.th ? (g.th < kTB ? g.th : kTB) : lead;
-        const int nrows = crb == 0 ? n_first : (g.th - crb < kTB ? g.th - crb : kTB);
-        issue(g, crb, ibuf);
+        cur_rec[0] = make_int4(box_unit<T, MIXED>(g), g.y0 - g.r, g.th, n_first);
+        cur_rec[1] = make_int4(g.f, width_of(g), 0, 0);
+    };
+    auto request_next = [&]() {
+        if (!cvalid) return;
+        const int4 ra = cur_rec[0], rb2 = cur_rec[1]; /* unit, first tile row, tile rows, rows of block 0; frame, width */
+        const int nrows = crb == 0 ? ra.w : (ra.z - crb < kTB ? ra.z - crb : kTB);
+        /* the box starts at the 16-byte unit that holds the stream's first byte (possibly left of
+         * the image: TMA fills what is outside with zeros) and at the first source row clamped
+         * into the image */
+        mbar_expect_tx(bar + ibuf, (uint32_t)((nq - (rb2.y << nq_shift)) * kQB * kTB));
+        tma_load_4d(smem_raw + ibuf * raw_bytes, &tmaps.m[rb2.y], bar + ibuf, 0, ra.x,
+                    fast_clamp(ra.y + crb, 0, H - 1), rb2.x);
         ibuf ^= nbuf - 1;
         crb += nrows;
-        if (crb >= g.th) { /* on to the following item */
+        if (crb >= ra.z) { /* on to the following item */
             crb = 0;
             clead++;
-            cq = clead == 1 ? q_nxt : d_q;
             cvalid = (clead == 1 ? idx_nxt : d_idx) < n_items;
+            if (cvalid) cursor_to(clead == 1 ? q_nxt : d_q);
         }
     };
-    if (tid == 0)
+    if (tid == 0) {
+        if (cvalid) cursor_to(q_cur);
         for (int i = 0; i < nbuf; i++) request_next();
+    }
 
     int bc = 0; /* blocks this CTA has been through: buffer bc % nbuf, its phase (bc / nbuf) & 1 */
     int wslot = 0, par = 0, item_no = 0;
