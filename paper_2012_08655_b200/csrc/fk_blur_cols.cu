@@ -129,6 +129,28 @@ template <> struct cols_px<float> {
     static __device__ __forceinline__ float store(float v) { return v; }
 };
 
+/* One RGB pixel of a V task to the output row, if the row exists: rounded unconditionally and
+ * stored under a predicate -- as a branch around the nine instructions of a row the guard
+ * cost three more per row (BSSY / BRA / BSYNC), eight rows per task. */
+__device__ __forceinline__ void store_px_if(bool ok, uint8_t *p, const float (&v)[kC])
+{
+    uint32_t a, b, c; /* convolve.py:15, as cols_px<uint8_t>::store, kept as the 32-bit cvt results */
+    asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(a) : "f"(fmaf(v[0], kOutScale, 0.5f)));
+    asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(b) : "f"(fmaf(v[1], kOutScale, 0.5f)));
+    asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(c) : "f"(fmaf(v[2], kOutScale, 0.5f)));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.u8 [%1], %2;\n\t"
+                 "@p st.global.u8 [%1+1], %3;\n\t@p st.global.u8 [%1+2], %4;\n\t}" ::"r"((uint32_t)ok),
+                 "l"(p), "r"(a), "r"(b), "r"(c)
+                 : "memory");
+}
+__device__ __forceinline__ void store_px_if(bool ok, float *p, const float (&v)[kC])
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.f32 [%1], %2;\n\t"
+                 "@p st.global.f32 [%1+4], %3;\n\t@p st.global.f32 [%1+8], %4;\n\t}" ::"r"((uint32_t)ok),
+                 "l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2])
+                 : "memory");
+}
+
 /* convert_rows_vec (fk_stage.cuh) with the scaled conversion */
 template <int NP>
 __device__ __forceinline__ void convert_rows_vec_s(const uint32_t *__restrict__ rp0,
@@ -458,6 +480,7 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
     const uint32_t ring_s = smem_u32(ring), tile_s = smem_u32(tile);
 
     const int W = pd.width, H = pd.height;
+    const uint32_t row_bytes = (uint32_t)(W * kC) * (uint32_t)sizeof(T); /* bytes between image rows */
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const fk_class_list list = fk_list_of(pd, klass);
@@ -772,15 +795,12 @@ fk_blur_cols(const __grid_constant__ CUtensorMap tmap, fk_plan_dev pd,
                         float acc[kRV][C];
                         v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
                                   4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, zpad, acc);
-                        T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px;
+                        const uint64_t ob = reinterpret_cast<uint64_t>(
+                            dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px);
 #pragma unroll
-                        for (int j = 0; j < kRV; j++) {
-                            if (gi * kRV + j < fh) {
-#pragma unroll
-                                for (int k = 0; k < C; k++) op[k] = cols_px<T>::store(acc[j][k]);
-                            }
-                            op += (size_t)W * C;
-                        }
+                        for (int j = 0; j < kRV; j++) /* row j: one 32 x 32 -> 64-bit multiply-add */
+                            store_px_if(gi * kRV + j < fh,
+                                        reinterpret_cast<T *>(ob + (uint64_t)row_bytes * (uint64_t)j), acc[j]);
                     }
                 }
             }
@@ -1113,6 +1133,7 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     const uint32_t ring_s = smem_u32(ring);
 
     const int W = pd.width, H = pd.height;
+    const uint32_t row_bytes = (uint32_t)(W * kC) * (uint32_t)sizeof(T); /* bytes between image rows */
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const fk_class_list list = fk_list_of(pd, klass);
@@ -1390,15 +1411,12 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
                         float acc[kRV][C];
                         v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
                                   4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, zpad, acc);
-                        T *op = dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px;
+                        const uint64_t ob = reinterpret_cast<uint64_t>(
+                            dst + ((size_t)(y0 + gi * kRV) * W + x0) * C + kSegF * warp + C * px);
 #pragma unroll
-                        for (int j = 0; j < kRV; j++) {
-                            if (gi * kRV + j < fh) {
-#pragma unroll
-                                for (int k = 0; k < C; k++) op[k] = cols_px<T>::store(acc[j][k]);
-                            }
-                            op += (size_t)W * C;
-                        }
+                        for (int j = 0; j < kRV; j++) /* row j: one 32 x 32 -> 64-bit multiply-add */
+                            store_px_if(gi * kRV + j < fh,
+                                        reinterpret_cast<T *>(ob + (uint64_t)row_bytes * (uint64_t)j), acc[j]);
                     }
                 }
             }
