@@ -1112,7 +1112,7 @@ template <typename T, int MINB, bool MIXED>
 __global__ void __launch_bounds__(kThreads, MINB)
 fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__restrict__ in,
             T *__restrict__ out, int klass, int wts_floats, int nq, int nq_shift, int icap, int ipitch,
-            int nbuf)
+            int nbuf, uint32_t icap_rcp)
 {
     constexpr int C = kC;
     constexpr bool kBytes = sizeof(T) == 1;
@@ -1406,8 +1406,8 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
                 for (int t = lane; t < ntask; t += 32) {
                     const int gi = vdone + (t >> 3), px = t & 7;
                     if (px < npx) {
-                        int r0 = gi * kRV;
-                        while (r0 >= icap) r0 -= icap;
+                        /* 8 gi mod icap by the reciprocal (exact: 8 gi * icap < 2^32) */
+                        const int r0 = gi * kRV - (int)__umulhi((uint32_t)(gi * kRV), icap_rcp) * icap;
                         float acc[kRV][C];
                         v_task_px(ring_s + 4u * (uint32_t)((kSegF * warp + C * px) * ipitch),
                                   4u * (uint32_t)ipitch, r0, icap, smem_u32(w_cur), nchunk, zpad, acc);
@@ -1599,7 +1599,8 @@ cudaError_t launch_tma(fk_handle *h, const fk_plan_dev &pd, int klass, const voi
     }
     const int grid = h->prop.multiProcessorCount * occ;
     kernel<<<grid, kThreads, smem, s>>>(maps, pd, (const T *)in, (T *)out, klass, wts_floats, nq,
-                                        nq_shift, icap, ipitch, nbuf);
+                                        nq_shift, icap, ipitch, nbuf,
+                                        (uint32_t)((0x100000000ull + (uint32_t)icap - 1) / (uint32_t)icap));
     *taken = true;
     return cudaGetLastError();
 }
