@@ -303,6 +303,8 @@ int fk_plan_create(fk_handle *h, int width, int height, int fragment_size, int m
         return fk_cuda_fail(h, e, "cudaMalloc(plan)");
     }
     d.taps = h->lut32;
+    d.y_lo = 0;
+    d.y_hi = 0x7fffffff;
     *out = p;
     return FK_OK;
 }
@@ -698,9 +700,24 @@ int fk_set_kernel_variant(fk_handle *h, int variant)
 int64_t fk_launch_count(const fk_handle *h) { return h ? h->launches : 0; }
 
 /* ------------------------------------------------------------------- request graph */
+/*
+ * One gaze-contingent frame as one CUDA-graph launch: fixation (pinned host memory, read by the
+ * plan kernel) -> plan -> render -> frame to pinned host memory.  The device-to-host copy of a
+ * 1080p frame (6.2 MB at the ~58 GB/s of the link: 0.107 ms) is half of a request, so the frame
+ * is rendered in TWO BANDS and the copy of the upper band runs under the render of the lower
+ * one: two plans of the same fixation, planned side by side, whose kernels emit only the
+ * rectangles that start in their band (fk_plan_dev::y_lo / y_hi) -- every pixel above the split
+ * row belongs to a rectangle that starts above it, so those rows are final once the upper
+ * band's launches are done.  FK_REQUEST_SPLIT (percent of the rows in the upper band; 0: one
+ * band) is read at creation; small frames are not split.
+ */
 struct fk_request {
     fk_handle *h = nullptr;
     fk_plan *p = nullptr;
+    fk_plan *p_low = nullptr;        /* plan of the lower band (owned) */
+    int32_t *info_low = nullptr;     /* device scratch its plan kernel reports to */
+    cudaStream_t s_plan = nullptr;   /* capture only: the lower band's plan */
+    cudaStream_t s_copy = nullptr;   /* capture only: the upper band's copy */
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     double *fix_host = nullptr;   /* pinned, 2 doubles */
@@ -713,6 +730,10 @@ int fk_request_destroy(fk_request *r)
     if (r->h) cudaSetDevice(r->h->device);
     if (r->exec) cudaGraphExecDestroy(r->exec);
     if (r->graph) cudaGraphDestroy(r->graph);
+    if (r->s_plan) cudaStreamDestroy(r->s_plan);
+    if (r->s_copy) cudaStreamDestroy(r->s_copy);
+    fk_plan_destroy(r->p_low);
+    cudaFree(r->info_low);
     cudaFreeHost(r->fix_host);
     cudaFreeHost(r->info_host);
     delete r;
@@ -731,51 +752,101 @@ int fk_request_create(fk_handle *h, fk_plan *p, const fk_params *prm, const void
         return fk_fail(h, FK_EINVAL, "a request is captured on a stream of its own, not the default stream");
     FK_CUDA(h, cudaSetDevice(h->device));
     const int W = p->d.width, H = p->d.height;
-    const size_t frame_bytes = (size_t)W * H * channels * (is_f32 ? 4 : 1);
+    const size_t row_bytes = (size_t)W * channels * (is_f32 ? 4 : 1);
+    const size_t frame_bytes = row_bytes * H;
     fk_request *r = new fk_request();
     r->h = h;
     r->p = p;
+    /* FK_REQUEST_PARTS (tuning runs): bit 0 plan, 1 render, 2 frame copy, 3 plan summary */
+    const char *pe = getenv("FK_REQUEST_PARTS");
+    const int parts = pe ? atoi(pe) : 15;
+    /* rows of the upper band: 55 % (1080p: 0.227 ms per request with one band, 0.211 / 0.207 /
+     * 0.207 / 0.213 ms with 40 / 50 / 60 / 70 %) -- the upper band's render is what no copy hides,
+     * the lower band's has to fit under the upper band's copy */
+    const char *se = getenv("FK_REQUEST_SPLIT");
+    const int split_pct = se ? atoi(se) : 55;
+    int y_split = 0;
+    if (out_host && parts == 15 && split_pct > 0 && split_pct < 100 && frame_bytes >= (1u << 20))
+        y_split = (int)((long long)H * split_pct / 100);
     cudaError_t e = cudaHostAlloc(&r->fix_host, 2 * sizeof(double), cudaHostAllocDefault);
     if (e == cudaSuccess)
         e = cudaHostAlloc(&r->info_host, (16 + (size_t)p->d.cap) * sizeof(int32_t), cudaHostAllocDefault);
+    if (e == cudaSuccess && y_split > 0) e = cudaMalloc(&r->info_low, (16 + (size_t)p->d.cap) * sizeof(int32_t));
+    if (e == cudaSuccess && y_split > 0) e = cudaStreamCreateWithFlags(&r->s_plan, cudaStreamNonBlocking);
+    if (e == cudaSuccess && y_split > 0) e = cudaStreamCreateWithFlags(&r->s_copy, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         fk_request_destroy(r);
-        return fk_cuda_fail(h, e, "cudaHostAlloc(request)");
+        return fk_cuda_fail(h, e, "request resources");
     }
     r->fix_host[0] = W / 2.0;
     r->fix_host[1] = H / 2.0;
     memset(r->info_host, 0, (16 + (size_t)p->d.cap) * sizeof(int32_t));
+    int rc = FK_OK;
+    if (y_split > 0) rc = fk_plan_create(h, W, H, p->d.fragment, 1, &r->p_low);
+    fk_plan *pl = r->p_low;
     /* one plain run first: it validates the arguments, grows the tap table to the longest filter
      * a fixation on the device can need and sets every kernel attribute -- nothing of which may
      * happen inside a capture */
-    int rc = fk_plan_model(p, prm, 1, r->fix_host, 0, stream);
+    if (rc == FK_OK) rc = fk_plan_model(p, prm, 1, r->fix_host, 0, stream);
     if (rc == FK_OK) rc = fk_plan_model(p, prm, 1, p->fix_dev, 1, stream);
+    if (rc == FK_OK && pl) rc = fk_plan_model(pl, prm, 1, p->fix_dev, 1, stream);
     if (rc == FK_OK) rc = fk_render_any(h, p, in_dev, out_dev, 1, channels, is_f32, stream);
     if (rc == FK_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = fk_fail(h, FK_ECUDA, "request warm-up failed");
     if (rc != FK_OK) {
         fk_request_destroy(r);
         return rc;
     }
-    e = cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed);
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}; /* fork, lower plan done, upper band rendered / copied */
+    for (int i = 0; i < 3 && pl && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) {
+        for (cudaEvent_t v : ev)
+            if (v) cudaEventDestroy(v);
         fk_request_destroy(r);
         return fk_cuda_fail(h, e, "cudaStreamBeginCapture");
     }
-    /* FK_REQUEST_PARTS (tuning runs): bit 0 plan, 1 render, 2 frame copy, 3 plan summary */
-    const char *pe = getenv("FK_REQUEST_PARTS");
-    const int parts = pe ? atoi(pe) : 15;
-    if (parts & 1) {
+    if (pl) { /* the lower band's plan, side by side with the upper band's */
+        e = cudaEventRecord(ev[0], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(r->s_plan, ev[0], 0);
+        if (e == cudaSuccess) {
+            pl->d.y_lo = y_split;
+            pl->request_info = r->info_low;
+            rc = fk_plan_model(pl, prm, 1, r->fix_host, 1, r->s_plan);
+            pl->request_info = nullptr;
+            pl->d.y_lo = 0;
+        }
+        if (e == cudaSuccess && rc == FK_OK) e = cudaEventRecord(ev[1], r->s_plan);
+    }
+    if (e == cudaSuccess && rc == FK_OK && (parts & 1)) {
         /* pinned host memory is mapped into the device's address space (unified addressing):
          * the plan kernel reads the fixation from it and writes the plan summary to it */
         p->request_info = (parts & 8) ? r->info_host : nullptr;
+        if (pl) p->d.y_hi = y_split;
         rc = fk_plan_model(p, prm, 1, r->fix_host, 1, stream);
+        p->d.y_hi = 0x7fffffff;
         p->request_info = nullptr;
     }
     if (e == cudaSuccess && rc == FK_OK && (parts & 2))
         rc = fk_render_any(h, p, in_dev, out_dev, 1, channels, is_f32, stream);
-    if (e == cudaSuccess && rc == FK_OK && out_host && (parts & 4))
+    if (pl && e == cudaSuccess && rc == FK_OK) {
+        /* rows [0, y_split) are final: their copy runs beside the lower band's render */
+        e = cudaEventRecord(ev[2], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(r->s_copy, ev[2], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out_host, out_dev, row_bytes * y_split, cudaMemcpyDeviceToHost, r->s_copy);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2], r->s_copy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[1], 0);
+        if (e == cudaSuccess) rc = fk_render_any(h, pl, in_dev, out_dev, 1, channels, is_f32, stream);
+        if (e == cudaSuccess && rc == FK_OK)
+            e = cudaMemcpyAsync((char *)out_host + row_bytes * y_split, (const char *)out_dev + row_bytes * y_split,
+                                row_bytes * (H - y_split), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2], 0);
+    } else if (e == cudaSuccess && rc == FK_OK && out_host && (parts & 4)) {
         e = cudaMemcpyAsync(out_host, out_dev, frame_bytes, cudaMemcpyDeviceToHost, s);
+    }
     cudaError_t e2 = cudaStreamEndCapture(s, &r->graph); /* always: leaves the stream usable */
+    for (cudaEvent_t v : ev)
+        if (v) cudaEventDestroy(v);
     if (rc == FK_OK && e != cudaSuccess) rc = fk_cuda_fail(h, e, "request capture");
     if (rc == FK_OK && e2 != cudaSuccess) rc = fk_cuda_fail(h, e2, "cudaStreamEndCapture");
     if (rc == FK_OK) {

@@ -116,6 +116,8 @@ struct fk_plan_dev {
     int mixed;           /* emit mixed items (FK_ITEM_MIXED) for groups of cells that differ */
     int canonical;       /* taps are the canonical table: the filter of radius r starts at r * r */
     int self_zero;       /* one-frame plans: the plan kernel zeroes `counters` itself (no memset node) */
+    int y_lo, y_hi;      /* only rectangles whose first row lies in [y_lo, y_hi) become items (a request
+                            renders a frame in two bands from two plans, fk_request_create) */
     int32_t *info_out;   /* optional host-mapped words the plan kernel fills for frame 0:
                             [0, 8) meta, [8] rejected fixations, [16, 16 + cells) tap counts */
     size_t items_cap;    /* entries per class list: max_frames * cap * nsub_x * nsub_y */

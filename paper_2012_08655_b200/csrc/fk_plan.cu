@@ -202,7 +202,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
         fh = y1 - ry0;
         fw = fw > FK_RECT ? FK_RECT : fw;
         fh = fh > FK_STRIP_ROWS ? FK_STRIP_ROWS : fh;
-        return fw > 0 && fh > 0;
+        return fw > 0 && fh > 0 && ry0 >= pd.y_lo && ry0 < pd.y_hi;
     };
 
     /* which end of its class list a strip goes to (fk_class_list, fk_internal.h): tall strips to
@@ -265,6 +265,7 @@ __device__ void fk_emit_items(const fk_plan_dev &pd, int f, int ncells, const CT
 __device__ void fk_emit_copy_through(const fk_plan_dev &pd, int f, bool count_bad)
 {
     const int W = pd.width, H = pd.height, tid = threadIdx.x;
+    if (pd.y_lo > 0) return; /* the plan of a request's lower band: the upper band's plan copies the frame */
     const int ncx = (W + 254) / 255, ncy = (H + 2046) / 2047;
     if (ncx * ncy <= pd.cap) {
         __shared__ int s_base;

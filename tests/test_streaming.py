@@ -133,6 +133,45 @@ def test_frame_request_graph_equals_foveate_float32_and_reports_plan():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("split", ["0", "30", "55"])
+def test_frame_request_in_two_bands_equals_foveate(split, monkeypatch):
+    """A request renders frames of a megabyte and more in two bands from two plans so that the
+    copy of the upper band runs under the render of the lower one (fk_request_create,
+    FK_REQUEST_SPLIT): whatever the split row, the frame on the device and in pinned host memory
+    equals foveate_batch -- fixations above, below and on the split row, RGB and gray."""
+    import torch
+    from paper_2012_08655_b200.engine import DevicePlan, FrameRequest, get_engine, pinned_empty
+
+    monkeypatch.setenv("FK_REQUEST_SPLIT", split)
+    rng = np.random.default_rng(21)
+    eng = get_engine(0)
+    for shape, F in (((1080, 1920, 3), 32), ((720, 1600, 1), 32), ((600, 800, 3), 16)):
+        h, w, _ = shape
+        frame = torch.from_numpy(rng.integers(0, 256, shape, dtype=np.uint8)).cuda()
+        out = torch.empty_like(frame)
+        host = pinned_empty(shape, np.uint8)
+        params = fk.FoveationParams(fragment_size=F)
+        plan = DevicePlan(eng, (w, h), F, 1)
+        stream = torch.cuda.Stream()
+        req = FrameRequest(eng, plan, params, frame, out, host, stream)
+        try:
+            ys = h * int(split) // 100
+            for (x, y) in [(w / 2.0, h / 2.0), (3.0, 2.0), (w - 1.0, h - 1.0), (w / 3.0, float(ys)),
+                           (w / 3.0, max(ys - 1.0, 0.0))]:
+                out.zero_()
+                host[...] = 0
+                req.launch(x, y)
+                stream.synchronize()
+                ref = fk.foveate_batch(frame[None], np.asarray([[x, y]]), params)[0]
+                assert torch.equal(out, ref), (shape, split, x, y)
+                assert np.array_equal(host, ref.cpu().numpy()), (shape, split, x, y)
+                assert req.info()["shift"] == tuple(fk.compute_fragment_shift((x, y), F))
+        finally:
+            req.close()
+            plan.close()
+
+
+@pytest.mark.gpu
 def test_stream_single_channel_image():
     """Gray sources go through the row-partitioned kernel inside the request graph."""
     rng = np.random.default_rng(12)
