@@ -1127,7 +1127,8 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     uint64_t *hbar = bar + 2;                                                   /* [2] H pass done */
     int *slot_idx = reinterpret_cast<int *>(bar + 4);                 /* [2] */
     uint4 *slot_desc = reinterpret_cast<uint4 *>(bar + 6);            /* [2], 16-byte aligned */
-    int4 *cur_rec = reinterpret_cast<int4 *>(bar + 12);               /* [2]: thread 0's request cursor */
+    int4 *cur_state = reinterpret_cast<int4 *>(bar + 10);             /* the request cursor: tile row, item, valid, buffer */
+    int4 *cur_rec = reinterpret_cast<int4 *>(bar + 12);               /* [2]: what its item's requests share */
     float *wts = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(bar) + 128);
     float *ring = wts + kWarps * 3 * wts_floats;
     const uint32_t ring_s = smem_u32(ring);
@@ -1167,9 +1168,9 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     };
 
     /* Items: the first two are blockIdx and blockIdx + grid; every further one is drawn by
-     * thread 0 from the class's cursor when it starts an item, published (index and
-     * descriptor) in shared memory before its next TMA issue, and picked up by everybody
-     * after the first "bytes landed" wait of the following item. */
+     * thread 0 from the class's cursor, published (index and descriptor) in shared memory one
+     * item after it was drawn -- its descriptor has long arrived by then -- and picked up by
+     * everybody after the first "bytes landed" wait of the following item. */
     int idx = (int)blockIdx.x, idx_nxt = idx + stride;
     uint4 q_cur = load_item(idx);
     uint4 q_nxt = load_item(idx_nxt);
@@ -1184,19 +1185,23 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
     if (idx < n_items) fill_taps(q_cur, 0);
     __syncthreads();
 
-    /* Thread 0's request cursor: the block to fetch next -- tile row `crb` of the item whose
-     * request record lies in shared memory -- runs nbuf blocks ahead of the H pass and `clead`
-     * items ahead of the item loop (every item has at least two blocks, so at most two: the next
-     * item, or the one drawn for after it).  The hand-over of a raw buffer is the one serial
-     * step of the CTA (warp 0 waits for the other warps' H passes, then thread 0 requests the
-     * next block while 31 lanes idle), so everything a request needs that does not change from
-     * block to block -- box unit and width, frame, first tile row, tile rows, rows of the first
-     * block -- is worked out once per item and kept as a 32-byte record that only thread 0
-     * writes and reads. */
+    /* The request cursor: the block to fetch next -- tile row `crb` of item number `citem` of this
+     * CTA -- runs nbuf blocks ahead of the H pass, at most two items ahead of the block that is
+     * handed over (every item has at least two blocks).  It lives in shared memory, because the
+     * hand-over of a raw buffer ROTATES through the warps: the warp on duty waits until every
+     * warp is through the buffer's H pass, and its lane 0 requests the block nbuf ahead while
+     * its other lanes idle -- ~860 cycles of a ~9 300-cycle block (a chain of dependent
+     * instructions issued among eleven other warps).  With warp 0 on duty at every block the
+     * CTA ran at warp 0's pace and the other three warps waited for bytes 16 % of their time
+     * (clock64 around the waits, profiles/README.md).  What the requests of an item share
+     * -- box unit and width, frame, first tile row, tile rows, rows of the first block -- is
+     * worked out once per item (cur_rec).  Order: a hand-over follows the arrivals of all warps
+     * at the buffer's hbar (release / acquire), the warp on duty at the next block is one of
+     * them, and the bytes a request brings are awaited through the expect_tx arrival of its
+     * lane 0 -- so the cursor, and the slots thread 0 publishes drawn items in, are seen in
+     * order by everybody who reads them. */
     int d_idx = n_items;
     uint4 d_q = none;
-    bool cvalid = idx < n_items;
-    int crb = 0, clead = 0, ibuf = 0;
     auto cursor_to = [&](const uint4 q) {
         const item_geo g = decode_item<C>(q, W);
         const int lead = (2 * g.r) & (kTB - 1);
@@ -1204,41 +1209,43 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
         cur_rec[0] = make_int4(box_unit<T, MIXED>(g), g.y0 - g.r, g.th, n_first);
         cur_rec[1] = make_int4(g.f, width_of(g), 0, 0);
     };
-    auto request_next = [&]() {
-        if (!cvalid) return;
+    /* by lane 0 of the warp on duty; item_no_ / par_: the item of the block that is handed over */
+    auto request_next = [&](int item_no_, int par_, int idx_nxt_, const uint4 &q_nxt_) {
+        int4 st = *cur_state; /* crb, citem, valid, buffer */
+        if (!st.z) return;
         const int4 ra = cur_rec[0], rb2 = cur_rec[1]; /* unit, first tile row, tile rows, rows of block 0; frame, width */
-        const int nrows = crb == 0 ? ra.w : (ra.z - crb < kTB ? ra.z - crb : kTB);
+        const int nrows = st.x == 0 ? ra.w : (ra.z - st.x < kTB ? ra.z - st.x : kTB);
         /* the box starts at the 16-byte unit that holds the stream's first byte (possibly left of
          * the image: TMA fills what is outside with zeros) and at the first source row clamped
          * into the image */
-        mbar_expect_tx(bar + ibuf, (uint32_t)((nq - (rb2.y << nq_shift)) * kQB * kTB));
-        tma_load_4d(smem_raw + ibuf * raw_bytes, &tmaps.m[rb2.y], bar + ibuf, 0, ra.x,
-                    fast_clamp(ra.y + crb, 0, H - 1), rb2.x);
-        ibuf ^= nbuf - 1;
-        crb += nrows;
-        if (crb >= ra.z) { /* on to the following item */
-            crb = 0;
-            clead++;
-            cvalid = (clead == 1 ? idx_nxt : d_idx) < n_items;
-            if (cvalid) cursor_to(clead == 1 ? q_nxt : d_q);
+        mbar_expect_tx(bar + st.w, (uint32_t)((nq - (rb2.y << nq_shift)) * kQB * kTB));
+        tma_load_4d(smem_raw + st.w * raw_bytes, &tmaps.m[rb2.y], bar + st.w, 0, ra.x,
+                    fast_clamp(ra.y + st.x, 0, H - 1), rb2.x);
+        st.w ^= nbuf - 1;
+        st.x += nrows;
+        if (st.x >= ra.z) { /* on to the following item: the next one, or the one after it */
+            st.x = 0;
+            st.y++;
+            const bool nxt = st.y - item_no_ == 1;
+            st.z = (nxt ? idx_nxt_ : slot_idx[par_]) < n_items;
+            if (st.z) cursor_to(nxt ? q_nxt_ : slot_desc[par_]);
         }
+        *cur_state = st;
     };
     if (tid == 0) {
-        if (cvalid) cursor_to(q_cur);
-        for (int i = 0; i < nbuf; i++) request_next();
+        *cur_state = make_int4(0, 0, idx < n_items, 0);
+        if (idx < n_items) {
+            cursor_to(q_cur);
+            for (int i = 0; i < nbuf; i++) request_next(0, 0, idx_nxt, q_nxt);
+            /* item 2 of this CTA: published when item 0 has its first bytes */
+            d_idx = 2 * stride + atomicAdd(cursor, 1);
+            d_q = load_item(d_idx);
+        }
     }
 
     int bc = 0; /* blocks this CTA has been through: buffer bc % nbuf, its phase (bc / nbuf) & 1 */
     int wslot = 0, par = 0, item_no = 0;
     for (; idx < n_items; idx = idx_nxt, q_cur = q_nxt, wslot ^= 1, par ^= 1, item_no++) {
-        /* thread 0: draw the item after the next and start fetching its descriptor */
-        bool d_pending = false;
-        if (item_no > 0 && clead > 0) clead--;
-        if (tid == 0) {
-            d_idx = 2 * stride + atomicAdd(cursor, 1);
-            d_q = load_item(d_idx);
-            d_pending = true;
-        }
         const float *w_cur = wts + (warp * 3 + wslot) * wts_floats; /* taps, V pass */
         /* H pass: its own copy -- scaled by 2^120 for uint8 frames (bytes_to_float4_s);
          * padded with zf zeros in front for float32 frames (h_float) */
@@ -1293,6 +1300,7 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
             const uint32_t phase = (uint32_t)((nbuf == 2 ? bc >> 1 : bc) & 1);
             unsigned char *raw = smem_raw + buf * raw_bytes;
             const uint32_t raw_s = smem_u32(raw);
+            const int duty = bc & (kWarps - 1); /* the warp that hands this block's buffer over */
             bc++;
             mbar_wait(bar + buf, phase); /* the block's bytes have landed */
             FK_DEBUG_CTA_SYNC();
@@ -1303,6 +1311,17 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
                     have_next = idx_nxt < n_items;
                 }
                 if (have_next) fill_taps(q_nxt, wslot ^ 1);
+                if (tid == 0) {
+                    /* The item after the next one -- drawn an item ago, its descriptor is here --
+                     * goes into this item's slot, and the one after it is drawn.  The slot is
+                     * free: these bytes were requested when every warp was through a block of
+                     * the previous item, hence past its own reading of the slot (one item ago)
+                     * and past every hand-over that read it (two items ago). */
+                    slot_idx[par] = d_idx;
+                    slot_desc[par] = d_q;
+                    d_idx = 2 * stride + atomicAdd(cursor, 1);
+                    d_q = load_item(d_idx);
+                }
             }
             if (!kBytes) {
                 if (box0 < 0 || skew + tw > W * C - box0) {
@@ -1371,21 +1390,11 @@ fk_blur_tma(const __grid_constant__ fk_tmaps tmaps, fk_plan_dev pd, const T *__r
             __syncwarp();
             FK_DEBUG_CTA_SYNC();
             if (lane == 0) mbar_arrive(hbar + buf); /* this warp is through with the raw bytes */
-            if (warp == 0) {
-                /* every warp is through with this buffer: publish the drawn item, then request
-                 * the block nbuf ahead into it */
+            if (warp == duty) {
+                /* every warp is through with this buffer: request the block nbuf ahead into it */
                 mbar_wait(hbar + buf, phase);
-                if (lane == 0) {
-                    if (d_pending) {
-                        slot_idx[par] = d_idx;
-                        slot_desc[par] = d_q;
-                        d_pending = false;
-                        __threadfence_block(); /* performed before the TMA request below: the
-                                                  other warps read the slot after they have
-                                                  seen bytes that request brought in */
-                    }
-                    request_next();
-                }
+                if (lane == 0) request_next(item_no, par, idx_nxt, q_nxt);
+                __syncwarp();
             }
             rbm += nrows;
             while (rbm >= icap) rbm -= icap;
