@@ -1,9 +1,16 @@
+"""Per-warp wait shares of fk_blur_tma on the headline batch.  Needs a libfovea.so built from a
+fk_blur_cols.cu instrumented with clock64 around mbar_wait(bar), mbar_wait(hbar) and request_next
+that exports fk_debug_wait_stats (16 counters: [0,4) cycles waiting for bytes per warp, [4,8) waits,
+[8] cycles waiting for hbar, [9] cycles in the request, [12,16) kernel cycles per warp); the shipped
+library has no such export (profiles/README.md holds the numbers measured with it)."""
 import ctypes as C, sys
 import numpy as np, torch
 sys.path.insert(0, ".")
 import paper_2012_08655_b200 as fk
 from paper_2012_08655_b200 import _native
 lib = _native.lib()
+if not hasattr(lib, "fk_debug_wait_stats"):
+    sys.exit("this libfovea.so is not the instrumented build")
 n = 256; H, W = 1080, 1920
 frames = torch.from_numpy(np.random.default_rng(0).integers(0, 256, (n, H, W, 3), dtype=np.uint8)).cuda()
 i = np.arange(n)
