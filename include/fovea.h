@@ -203,6 +203,12 @@ int64_t fk_launch_count(const fk_handle *h);
  *                      request; in_dev / out_dev are [H][W][C] device buffers, out_host (may be
  *                      NULL) pinned host memory of the same size.  The graph holds the class
  *                      launches of the longest filter any fixation inside the image can need.
+ *                      With out_host, frames of a megabyte and more are rendered in two
+ *                      bands (the rows above and below FK_REQUEST_SPLIT percent of the height,
+ *                      default 55, read at creation; 0: one band) from two plans of the same
+ *                      fixation, and the upper band travels to out_host while the lower one
+ *                      renders; out_dev and out_host hold the whole frame when the stream has
+ *                      been synchronised, whatever the split.
  *   fk_request_launch  queues one request for fixation (fx, fy) -- which must lie inside the
  *                      image, the caller clamps as service.py:58-63 does -- on `stream`.
  *   fk_request_info    pinned host words, valid once the stream has been synchronised:
