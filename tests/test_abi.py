@@ -153,3 +153,21 @@ def test_shard_range_partitions():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         fk.shard_range(10, 2, 2)
+
+
+def test_handover_protocol_model_holds_for_one_and_two_raw_buffers():
+    """tools/handover_model.py: the item slots, the request cursor and the rotating hand-over of
+    fk_blur_tma under random interleavings of its four warps -- no slot read before it holds the
+    wanted item, no cursor more than two items ahead, no wait without end -- for the buffer
+    counts the kernel uses; with a third buffer the model finds the read that precedes its
+    publication (why the kernel stops at two)."""
+    import importlib.util
+    import pathlib
+
+    path = pathlib.Path(__file__).resolve().parents[1] / "tools" / "handover_model.py"
+    spec = importlib.util.spec_from_file_location("handover_model", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.check(1, 2, 400) == []
+    assert mod.check(2, 2, 400) == []
+    assert mod.check(3, 4, 400) != []
