@@ -11,12 +11,13 @@ items ahead of a hand-over, and that nobody waits forever.
 Result: nbuf = 1 and 2 (what the kernel uses) hold with two slots; nbuf = 3 does not -- a warp
 can then be a whole two-block item ahead of thread 0 and read a slot before thread 0 has
 published it (the third raw buffer that was tried hung in the chunked host pipeline for this
-reason).  usage: python tools/handover_model.py [cases]"""
+reason); with every drawn item published three items ahead instead of two (`ahead` = 3, four
+slots) three buffers hold as well -- measured: no faster, not kept.  usage: python tools/handover_model.py [cases]"""
 import random
 import sys
 
 
-def run(nbuf, nitems, seed, nslots):
+def run(nbuf, nitems, seed, nslots, ahead=2):
     rng = random.Random(seed)
     blocks = [rng.choice([2, 2, 2, 3, 4, 6]) for _ in range(nitems)]
     item_of, first = [], []
@@ -29,7 +30,9 @@ def run(nbuf, nitems, seed, nslots):
     requested, handed = set(), set()
     pos = [(0, 0)] * 4          # per warp: (block, stage); stages: wait bytes, pick up / publish, H + arrive, duty, V
     arrived = [0] * nblk
-    drawn = [2]                 # thread 0 holds item 2 after the prologue
+    drawn = [ahead]             # thread 0 holds this item after the prologue
+    if ahead == 3:
+        slots[(0 - 1) % nslots] = 2   # the prologue publishes item 2 itself
 
     def request_next(item_no):
         if not cur["valid"]:
@@ -46,7 +49,7 @@ def run(nbuf, nitems, seed, nslots):
             if rel == 1:
                 n = item_no + 1
             else:
-                n = slots[item_no % nslots]
+                n = slots[(item_no + 2 - ahead) % nslots]
                 assert n == item_no + 2, ("hand-over read slot", n, "wanted", item_no + 2)
             cur["valid"] = n < nitems
 
@@ -70,7 +73,7 @@ def run(nbuf, nitems, seed, nslots):
         i = item_of[k]
         if st == 1 and k == first[i]:
             if i > 0:
-                s = slots[(i - 1) % nslots]
+                s = slots[(i + 1 - ahead) % nslots]
                 assert s == i + 1, ("pick-up read slot", s, "wanted", i + 1)
             if w == 0:
                 slots[i % nslots] = drawn[0]
@@ -84,11 +87,11 @@ def run(nbuf, nitems, seed, nslots):
     return "no progress"
 
 
-def check(nbuf, nslots, cases):
+def check(nbuf, nslots, cases, ahead=2):
     bad = []
     for seed in range(cases):
         try:
-            r = run(nbuf, random.Random(seed).randint(1, 12), seed, nslots)
+            r = run(nbuf, random.Random(seed).randint(1, 12), seed, nslots, ahead)
         except AssertionError as e:
             r = e.args[0]
         if r != "ok":
@@ -98,6 +101,7 @@ def check(nbuf, nslots, cases):
 
 if __name__ == "__main__":
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 3000
-    for nbuf, nslots in ((1, 2), (2, 2), (3, 4)):
-        bad = check(nbuf, nslots, cases)
-        print(f"nbuf {nbuf}, {nslots} slots: {cases - len(bad)} of {cases} ok" + (f"; first failure {bad[0]}" if bad else ""))
+    for nbuf, nslots, ahead in ((1, 2, 2), (2, 2, 2), (3, 4, 2), (3, 4, 3), (2, 4, 3), (1, 4, 3)):
+        bad = check(nbuf, nslots, cases, ahead)
+        print(f"nbuf {nbuf}, {nslots} slots, published {ahead} items ahead: {cases - len(bad)} of {cases} ok"
+              + (f"; first failure {bad[0]}" if bad else ""))
