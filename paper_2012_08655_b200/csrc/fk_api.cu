@@ -44,12 +44,11 @@ int fk_strip_rows_for(int n_frames, int width, int height)
     if (forced > 0) return forced < FK_STRIP_ROWS ? forced : FK_STRIP_ROWS;
     /* By the 32 x 32 pixel units of the batch (what the persistent CTAs have to share; 2 040 per
      * 1080p frame), measured with the tall strips drawn first: one 1080p frame streams fastest
-     * with 64-row strips, 4 with 128, 8 with 256 (0.57 of the roofline against 0.54 with 1 024),
-     * 16 to 64 with 512 (16 frames: 0.637 against 0.626 with 256), more with the tallest
-     * (tools/strip_sweep.sh). */
+     * with 64-row strips, 8-16 frames with 256 (0.54 of the roofline against 0.51 with 1 024 at
+     * 8 frames), 32 with 512, 64 and more with the tallest. */
     const long long cells = (long long)n_frames * ((width + FK_RECT - 1) / FK_RECT) *
                             ((height + FK_RECT - 1) / FK_RECT);
-    return cells >= 131072 ? FK_STRIP_ROWS : cells >= 24576 ? 512 : cells >= 8192 ? 256
+    return cells >= 131072 ? FK_STRIP_ROWS : cells >= 65536 ? 512 : cells >= 8192 ? 256
          : cells >= 4096 ? 128 : 64;
 }
 
